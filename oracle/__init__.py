@@ -68,6 +68,8 @@ def lib():
             "orc_source": (C.c_int, [pp, i64, d, pd]),
             "orc_exact": (C.c_int, [pp, d, pd]),
             "orc_ge_solve": (C.c_int, [i64, pd, pd]),
+            "orc_matvec": (C.c_int, [pp, i64, C.c_int, pd, pd]),
+            "orc_rhs_nodense": (C.c_int, [pp, i64, pd, pd]),
             "orc_solve": (C.c_int, [pp, pd]),
             "orc_solve_level": (C.c_int, [pp, i64, pd, pd]),
             "orc_l2": (d, [i64, d, pd]),
@@ -187,6 +189,23 @@ def rhs(p: Problem, j: int, U: np.ndarray) -> np.ndarray:
     g = np.zeros(p.n)
     cp = p.c()
     assert lib().orc_rhs(C.byref(cp), j, _pd(U), _pd(g)) == 0
+    return g
+
+
+def matvec(p: Problem, j: int, which: int, x: np.ndarray) -> np.ndarray:
+    """A^{(j+sigma)} x (which=0) or B^{(j+sigma)} x (which=1) without dense storage."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(p.n)
+    cp = p.c()
+    assert lib().orc_matvec(C.byref(cp), j, which, _pd(x), _pd(y)) == 0
+    return y
+
+
+def rhs_nodense(p: Problem, j: int, U: np.ndarray) -> np.ndarray:
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    g = np.zeros(p.n)
+    cp = p.c()
+    assert lib().orc_rhs_nodense(C.byref(cp), j, _pd(U), _pd(g)) == 0
     return g
 
 

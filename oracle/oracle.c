@@ -295,6 +295,61 @@ int orc_rhs(const orc_problem *p, int64_t j, const double *U, double *g) {
   return 0;
 }
 
+/* Matrix-free products with A^{(j+sigma)} (which = 0) or B^{(j+sigma)} (which = 1): the
+ * same entries as orc_assemble (eq3.2-eq3.3) generated row by row, O(n^2) time and O(n)
+ * memory, for sampled checks at sizes where the dense matrix does not fit.               */
+int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y) {
+  if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
+  const int64_t n = p->n;
+  const double h = (p->b - p->a) / (double)(n + 1);
+  const double tau = p->T / (double)p->M;
+  const double sigma = 1.0 - p->alpha / 2.0;
+  const double t = ((double)j + sigma) * tau;
+  const double gam = orc_eval_fn(p->gamma, t);
+  const double dp = orc_eval_fn(p->dplus, t), dm = orc_eval_fn(p->dminus, t);
+  const double hb = pow(h, p->beta);
+  const double eta = orc_eta(p->alpha, tau, j);
+  const double mu = (which == 0) ? -sigma : (1.0 - sigma);
+  double *omega = (double *)malloc(sizeof(double) * (size_t)(n + 2));
+  orc_wsgd(p->beta, n + 1, omega);
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t m = 0; m < n; ++m) {
+      double W = (i - m + 1 >= 0) ? omega[i - m + 1] : 0.0;
+      double WT = (m - i + 1 >= 0) ? omega[m - i + 1] : 0.0;
+      double Q = (m == i + 1) ? 1.0 : ((m == i - 1) ? -1.0 : 0.0);
+      s += (gam / (2.0 * h) * Q + dp / hb * W + dm / hb * WT) * x[m];
+    }
+    y[i] = eta * x[i] + mu * s;
+  }
+  free(omega);
+  return 0;
+}
+
+/* RHS of alg1 step 2 without dense storage (same arithmetic order as orc_rhs's sums). */
+int orc_rhs_nodense(const orc_problem *p, int64_t j, const double *U, double *g) {
+  if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
+  const int64_t n = p->n;
+  const double tau = p->T / (double)p->M;
+  const double sigma = 1.0 - p->alpha / 2.0;
+  const double kappa = pow(tau, -p->alpha) / tgamma(2.0 - p->alpha);
+  orc_matvec(p, j, 1, U + j * n, g);
+  if (j >= 1) {
+    double *c = (double *)malloc(sizeof(double) * (size_t)(j + 1));
+    orc_c_row(p->alpha, j, c);
+    for (int64_t s = 0; s <= j - 1; ++s) {
+      const double w = kappa * c[j - s];
+      for (int64_t i = 0; i < n; ++i) g[i] -= w * (U[(s + 1) * n + i] - U[s * n + i]);
+    }
+    free(c);
+  }
+  double *f = (double *)malloc(sizeof(double) * (size_t)n);
+  orc_source(p, j, ((double)j + sigma) * tau, f);
+  for (int64_t i = 0; i < n; ++i) g[i] += f[i];
+  free(f);
+  return 0;
+}
+
 int orc_solve_level(const orc_problem *p, int64_t j, const double *U, double *out) {
   if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
   const int64_t n = p->n;

@@ -62,6 +62,9 @@ int orc_source(const orc_problem *p, int64_t j, double t, double *f);
 int orc_exact(const orc_problem *p, double t, double *u);
 /* Gaussian elimination with partial pivoting; A destroyed. */
 int orc_ge_solve(int64_t n, double *A, double *x_inout);
+/* Matrix-free A (which=0) / B (which=1) product and RHS for large n (O(n) memory). */
+int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y);
+int orc_rhs_nodense(const orc_problem *p, int64_t j, const double *U, double *g);
 /* Full IDS run (alg1) with a direct solve per level: U[(M+1)][n]. */
 int orc_solve(const orc_problem *p, double *U);
 /* Same, but solve level j only from a given history (teacher forcing): out[n]. */

@@ -1,0 +1,114 @@
+// tsf_plan.h -- host planner of the per-level solver (no CUDA types; compiled by g++/nvcc).
+//
+// The planner validates problems, computes the O(M) scalar tables of the scheme
+// (Lemma 1 weights, eta_j, kappa), picks the thread-block-cluster
+// size, builds the integer FFT/task tables and lays out the caller's device workspace.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tsf.h"
+
+namespace tsf {
+
+constexpr int kThreads = 256;          // threads per CTA
+constexpr int kMaxLocal = 8192;        // max complex elements of the local FFT (128 KiB)
+constexpr int kNumVec = 11;            // u, Krylov work vectors, phi copy
+constexpr size_t kAlign = 256;
+
+// Vector slots inside the per-instance vector block (each n doubles).
+enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_PHI };
+
+// Plain-old-data parameters handed to every kernel by value.
+struct DevParams {
+  int64_t n, M;
+  int32_t B, C, K, src_kind, method, precond, maxit;
+  int32_t L1e, L1p, npe, npp;      // local FFT lengths and column-pair tasks per CTA
+  double tol;
+  double scale_e, scale_p;         // 1/(4L) folding of the real-FFT split and 1/L
+  double qscale_p;                 // Lambda_Q scale of the preconditioner: 1 or (n-1)/n
+  int32_t strang;                  // Strang midpoint correction active
+  int32_t twN;                     // twiddle table length (2n)
+  // shared tables
+  const void *tw;                  // double2[2n]: e^{-2 pi i e/(2n)}
+  const int32_t *slot_e, *slot_p;  // k1 -> slot of the local DIF output
+  const double *sq_e, *sq_p;       // sin tables in task order
+  int64_t *level;                  // device level counter
+  // per-instance block
+  char *inst;                      // base of instance 0
+  int64_t stride;                  // bytes between instances
+  int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st;
+};
+
+struct Plan {
+  int64_t n = 0, M = 0;
+  int32_t B = 0, C = 1, K = 0, src_kind = 0;
+  int32_t method = 0, precond = 0, maxit = 0;
+  double tol = 0;
+  int32_t L1e = 0, L1p = 0, npe = 0, npp = 0;
+  int64_t smem = 0;
+  // workspace layout (byte offsets from the workspace base)
+  size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
+  size_t off_level = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
+  int32_t scratch_batch = 0;
+  size_t stride = 0, total = 0;
+  int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st;
+};
+
+// Per-instance host tables (all doubles).
+struct InstTables {
+  double sigma = 0, kappa = 0, h = 0, tau = 0;
+  std::vector<double> lev;   // [M][4]: eta_j, gamma_j/(2h), d+_j/h^beta, d-_j/h^beta
+  std::vector<double> hwc;   // [M]: kappa * chat_m, chat_m = a_m + b_{m+1} - b_m (m >= 1)
+  std::vector<double> hwe;   // [M]: kappa * e_j,    e_j = a_j - b_j             (j >= 1)
+};
+
+// Error reporting shared with the C-ABI (thread-local message).
+void set_error(const std::string &msg);
+const char *last_error();
+
+bool is_pow2(int64_t v);
+int validate(const tsf_problem *p, int32_t B, const tsf_solver *s);
+int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *plan);
+int sample_points(const tsf_problem &p, double *x, double *t);
+int inst_tables(const tsf_problem &p, InstTables *out);
+
+// FFT integer tables (DESIGN.md R-fft).
+int fft_plan_radices(int64_t L, int32_t *plan);
+void fft_perm(int64_t L, int32_t *perm);
+int64_t fft_stage_twiddles(int64_t L, int s, int32_t *tw);
+
+#ifdef __CUDACC__
+#define TSF_HD __host__ __device__
+#else
+#define TSF_HD
+#endif
+
+// Column-pair task geometry: CTA r owns the column pairs
+// pi = r + i C (i < L1/(2C)) of the L1 x C four-step grid, pair (k1a, k1b) = (pi, L1 - pi),
+// or (0, L1/2) for pi = 0.  Bin of (task i, row k2, column ab) is k1 + L1 k2.
+TSF_HD inline int64_t task_bin(int64_t L1, int C, int r, int i, int k2, int ab) {
+  const int64_t pi = int64_t(r) + int64_t(i) * C;
+  const int64_t k1a = pi == 0 ? 0 : pi;
+  const int64_t k1b = pi == 0 ? L1 / 2 : L1 - pi;
+  return (ab ? k1b : k1a) + L1 * int64_t(k2);
+}
+// Task-order storage index of (r, k2, ab, i) for np tasks per CTA.
+TSF_HD inline int64_t task_index(int C, int np, int r, int k2, int ab, int i) {
+  return ((int64_t(r) * C + k2) * 2 + ab) * np + i;
+}
+// Permuted chunk layout: element e (natural order) of an n-vector lives at
+// r (n/C) + 2 m1 + (e & 1) with m = e/2 = C m1 + r, so CTA r owns a contiguous chunk of
+// packed complex values z_m = (x_{2m}, x_{2m+1}) with m = r mod C.
+TSF_HD inline int64_t perm_pos(int64_t n, int C, int64_t e) {
+  const int64_t m = e >> 1, r = m % C, m1 = m / C;
+  return r * (n / C) + 2 * m1 + (e & 1);
+}
+
+DevParams dev_params(const Plan &pl, char *ws);
+
+}  // namespace tsf

@@ -1,0 +1,371 @@
+"""Benchmark of the B200 per-level Toeplitz Krylov solver (arXiv 1603.00279 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A "step" is one full time-marching solve (all M levels: RHS with the history sum, the
+preconditioned Krylov solve, finalize) of the rank's batch, inputs resident in HBM.
+Default workload: BASELINE configs[2] "C3" (n = 2^14, M = 2^9, one instance per GPU:
+weak scaling over independent replicas).  --config C4 / C5 run the batched configs,
+sharded over ranks (strong scaling).  Prints ONE JSON line on rank 0.
+
+metric: FP64 precond-Krylov iterations/s & time levels/s (value = levels/s, whole job).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 precond-Krylov iters/s & time levels/s at N=2^14; achieved HBM GB/s"
+KRYLOV_UNITS = {"bicgstab": 26, "cgnr": 19}      # streamed units per iteration
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(n, M, iters_half_rows, method, src_units):
+    """SURVEY 8(d) model per instance: 8n (j + 3 + src + 8) compulsory/RHS bytes per level
+    plus 8n * units * I_j for the streamed Krylov iterations (I_j = iterations of level j)."""
+    units = KRYLOV_UNITS[method]
+    total = 0.0
+    for row in iters_half_rows:
+        for j in range(M):
+            total += 8.0 * n * (j + 3 + src_units + 8) + 8.0 * n * units * (row[j] / 2.0)
+    return total
+
+
+def build_instances(cfg, world, rank):
+    from paper_1603_00279_b200 import dist
+    from paper_1603_00279_b200.inputs import CONFIGS
+    insts = CONFIGS[cfg]()
+    if cfg in ("C1", "C2", "C3"):          # single-instance configs: one replica per rank (weak)
+        return insts, "weak", len(insts) * world
+    mine = [insts[i] for i in dist.shard(len(insts), world, rank)]
+    return mine, "strong", len(insts)
+
+
+# ------------------------------------------------------------------------------ oracle arm
+def oracle_problem(inst):
+    import oracle as O
+    shape = lambda fn: fn  # noqa: E731
+    # map the config's coefficient functions onto the oracle's shape enum
+    import numpy as np
+    t = np.array([0.1, 0.7])
+
+    def enc(fn):
+        v = np.asarray(fn(t), dtype=float) * np.ones(2)
+        if abs(v[0] - v[1]) < 1e-15:
+            return (O.CONST, float(v[0]))
+        for sh, g in ((O.ONE_PLUS_T, lambda s: 1 + s), (O.ONE_PLUS_T2, lambda s: 1 + s * s),
+                      (O.COS, np.cos), (O.SIN, np.sin), (O.T, lambda s: s)):
+            c = v[0] / g(t[0])
+            if abs(c * g(t[1]) - v[1]) < 1e-12 * max(1, abs(v[1])):
+                return (sh, float(c))
+        raise ValueError("coefficient not expressible for the oracle")
+    src = {"mms3": O.SRC_MMS3, "exa": O.SRC_EXA, "table": O.SRC_TABLE, "zero": O.SRC_ZERO}[inst.source]
+    del shape
+    return dict(alpha=inst.alpha, beta=inst.beta, gamma=enc(inst.gamma), dplus=enc(inst.dplus),
+                dminus=enc(inst.dminus), src=src)
+
+
+def oracle_rate(cfg):
+    """Oracle levels/s for `cfg`, from a bounded sample (10-30 s of CPU work) extrapolated
+    to the full size: dense GE is O(n^3) per factorization and O(n^2) per level."""
+    import numpy as np
+
+    import oracle as O
+    from paper_1603_00279_b200.inputs import CONFIGS
+    insts = CONFIGS[cfg]()
+    inst = insts[0]
+    kw = oracle_problem(inst)
+    n, M, B = inst.n, inst.M, len(insts)
+    const = all(kw[k][0] == O.CONST for k in ("gamma", "dplus", "dminus"))
+    ns = min(n, 1024 if const else 512)
+    ns = ns - 1 if ns == n else ns      # any n is fine for the oracle
+
+    def run(nn, MM):
+        p = O.Problem(n=nn, M=MM, **kw)
+        if p.src == O.SRC_TABLE:
+            p.f_table = np.ascontiguousarray(inst.f_table[:MM, :nn])
+        t0 = time.perf_counter()
+        O.solve(p)
+        return time.perf_counter() - t0
+    if const:     # LU reuse: 2 factorizations + per-level triangular solves
+        Ms = min(M, 64)
+        t2 = run(ns, 2)
+        tm = run(ns, Ms)
+        per_level = max((tm - t2) / (Ms - 2), 1e-9)
+        fact = max(t2 - 2 * per_level, 1e-9)
+        s = n / ns
+        full = fact * s**3 + M * per_level * s**2
+        sample = (f"oracle (dense GE, LU reuse) on {cfg} params at n={ns}: 2 levels {t2:.2f}s, "
+                  f"{Ms} levels {tm:.2f}s; extrapolated to n={n}, M={M} as fact*(n/ns)^3 + "
+                  f"M*level*(n/ns)^2 = {full:.1f}s per instance")
+    else:         # variable coefficients: one factorization per level
+        Ms = 4
+        tm = run(ns, Ms)
+        per_level = tm / Ms
+        s = n / ns
+        full = M * per_level * s**3
+        sample = (f"oracle (dense GE per level) on {cfg} params at n={ns}, {Ms} levels {tm:.2f}s; "
+                  f"extrapolated to n={n}, M={M} as M*level*(n/ns)^3 = {full:.1f}s per instance")
+    return M / full, sample, full * B
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    sample = ""
+    for _ in range(args.warmup):
+        oracle_rate(args.config)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        v, sample, _ = oracle_rate(args.config)
+        vals.append((v, time.perf_counter() - t0))
+    value = statistics.median(v for v, _ in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "levels/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.mean(t for _, t in vals), "higher_is_better": True,
+            "scaling": "weak" if args.config in ("C1", "C2", "C3") else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": {"workload": args.config},
+            "cpu_baseline": {"value": value, "unit": "levels/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "levels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "cgnr"])
+    ap.add_argument("--precond", default="strang", choices=["strang", "tchan", "none"])
+    ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1603_00279_b200 import tsf
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        tdist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    def allmax(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
+        return float(t.item())
+
+    insts, scaling, units_total = build_instances(args.config, world, rank)
+    n, M = insts[0].n, insts[0].M
+    solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster)
+    stream = torch.cuda.Stream(dev)
+    t_init0 = time.perf_counter()
+    s = tsf.Solver(insts, stream=stream, **solver_kw)
+    t_init = time.perf_counter() - t_init0
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
+
+    for _ in range(args.warmup):
+        s.reset()
+        s.solve()
+        rc = s.sync()
+        assert rc >= 0, rc
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters_total = 0.0
+    ms = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            s.reset()
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)                 # flush L2 between timed steps
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            ev[k][0].record(stream)
+            s.solve()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            ms.append(ev[k][0].elapsed_time(ev[k][1]))
+            rc = s.sync()
+            assert rc >= 0, rc
+    it_half, relres, status = s.stats()
+    iters_local = float(it_half.sum()) / 2.0
+    t_step_ms = allmax(statistics.mean(ms))
+    total_s = allmax(sum(ms) / 1000.0)
+    iters_job = allsum(iters_local)
+    levels_job = units_total * M
+    value = levels_job * args.steps / total_s
+    iters_per_s = iters_job * args.steps / total_s
+    src_units = 1 if insts[0].source == "table" else (4 if insts[0].source in ("mms3", "exa") else 0)
+    abytes = algorithmic_bytes(n, M, it_half, args.method, src_units)   # per launch, this rank
+    achieved = abytes / (statistics.mean(ms) / 1000.0) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{args.config}/{args.method}/{args.precond}")
+    except Exception:
+        pass
+
+    # ---- end to end through the public API: host inputs -> device, solve, results -> host
+    e2e = None
+    if not args.no_e2e:
+        e_ms = []
+        h2d = d2h = 0
+        for k in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            s2 = tsf.Solver(insts, stream=stream, workspace=s.workspace, **solver_kw)
+            s2.solve()
+            u = s2.solutions()
+            it2, rr2, st2 = s2.stats()
+            t1 = time.perf_counter()
+            h2d = s2.h2d_bytes
+            d2h = u.nbytes + it2.nbytes + rr2.nbytes + st2.nbytes
+            s2.close()
+            e_ms.append(allmax(t1 - t0))
+        e2e = {"value": levels_job / statistics.mean(e_ms), "unit": "levels/s",
+               "h2d_bytes_per_step": int(allsum(h2d)), "d2h_bytes_per_step": int(allsum(d2h))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample, _ = oracle_rate(args.config)
+        cpu = {"value": v, "unit": "levels/s", "cores": 1, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        info = s.info
+        line = {
+            "metric": METRIC, "value": value, "unit": "levels/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step_ms,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "n": n, "M": M, "instances": units_total,
+                       "method": args.method, "precond": args.precond, "cluster": info.cluster,
+                       "l2": "flushed between steps (512 MiB write)", "tol": 1e-12},
+            "krylov_iters_per_s": iters_per_s,
+            "mean_iters_per_level": iters_job / levels_job,
+            "init_s": t_init,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_solve (one launch = all M levels of the rank's batch)",
+                         "algorithmic_bytes_per_launch": abytes},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "max_relres": float(relres.max()),
+            "status_ok": bool((status == 0).all()),
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

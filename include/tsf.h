@@ -185,6 +185,9 @@ int tsf_debug_rhs(tsf_handle *h, int32_t inst, double *out);
 /* Overwrite the solution history of instance `inst` with host U[(j+1)][n] = u^0..u^j and
  * set the handle to level j (teacher forcing).  Every instance is moved to level j.    */
 int tsf_debug_set_history(tsf_handle *h, int32_t inst, int64_t j, const double *U);
+/* Section cycle counters of the profiling build (libtsf_prof.so; zeros otherwise):
+ * out[32] host, then cleared when reset != 0.                                          */
+int tsf_debug_prof(tsf_handle *h, uint64_t *out, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtsf.so")
+# TSF_LIB_VARIANT=prof selects the section-timer build (developer profiling only)
+LIB_PATH = os.path.join(HERE, "lib", "libtsf_prof.so" if os.environ.get("TSF_LIB_VARIANT") == "prof"
+                        else "libtsf.so")
 
 TSF_OK = 0
 TSF_W_MAXIT = 1
@@ -78,6 +80,7 @@ _SIGS = {
     "tsf_debug_spectra": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, PD, PD]),
     "tsf_debug_rhs": (C.c_int, [C.c_void_p, C.c_int32, PD]),
     "tsf_debug_set_history": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, PD]),
+    "tsf_debug_prof": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32]),
 }
 
 EXPORTED = tuple(_SIGS)

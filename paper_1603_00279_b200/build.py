@@ -1,40 +1,56 @@
-"""Build the sm_100a shared library libtsf.so in-tree (nvcc, FP64, -lineinfo)."""
+"""Build the sm_100a shared library libtsf.so in-tree (nvcc, FP64, -lineinfo).
+
+Translation units are compiled in parallel (one per thread-block-cluster size holds the
+solve-kernel instantiations), then linked with the static CUDA runtime.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "lib", "libtsf.so")
-SOURCES = ["tsf_plan.cpp", "tsf_capi.cu"]
+LIBDIR = os.path.join(HERE, "lib")
+LIB = os.path.join(LIBDIR, "libtsf.so")
+PROF_LIB = os.path.join(LIBDIR, "libtsf_prof.so")
+SOURCES = ["tsf_plan.cpp", "tsf_capi.cu"] + [f"tsf_solve_c{c}.cu" for c in (1, 2, 4, 8, 16)]
 HEADERS = ["tsf_plan.h", "tsf_kernels.cuh", os.path.join("..", "..", "include", "tsf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+def _compile(src: str, verbose: bool, profile: bool = False) -> str:
+    obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ("_prof.o" if profile else ".o"))
+    cmd = [NVCC, *FLAGS, *(["-DTSF_PROFILE"] if profile else []), "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """Build libtsf.so (or the section-timer variant libtsf_prof.so with profile=True)."""
+    lib = PROF_LIB if profile else LIB
+    if not force and not _stale(lib):
+        return lib
+    os.makedirs(LIBDIR, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose, profile), SOURCES))
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs])
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

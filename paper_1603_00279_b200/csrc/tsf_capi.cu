@@ -14,6 +14,15 @@
 
 using namespace tsf;
 
+namespace tsf {
+__global__ void k_advance(int64_t *level, int64_t by, int64_t M) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int64_t v = *level + by;
+    *level = v < M ? v : M;
+  }
+}
+}  // namespace tsf
+
 struct tsf_handle {
   Plan pl;
   DevParams dp;
@@ -196,12 +205,13 @@ __global__ void k_set_level(int64_t *level, int64_t v) {
 
 __global__ void k_dbg_fft(double2 *buf, int L, const double2 *tw, int twN, int inverse) {
   extern __shared__ __align__(16) unsigned char raw[];
-  double2 *A = reinterpret_cast<double2 *>(raw);
-  for (int e = threadIdx.x; e < L; e += blockDim.x) A[e] = buf[e];
+  const Smem sm = smem_view(raw, L, false, nullptr);
+  load_twiddles(sm, L, tw, twN);
+  for (int e = threadIdx.x; e < L; e += blockDim.x) sm.A[e] = buf[e];
   __syncthreads();
-  if (inverse) local_fft<true>(A, L, tw, twN);
-  else local_fft<false>(A, L, tw, twN);
-  for (int e = threadIdx.x; e < L; e += blockDim.x) buf[e] = A[e];
+  if (inverse) local_fft<true>(sm.A, L, sm, L);
+  else local_fft<false>(sm.A, L, sm, L);
+  for (int e = threadIdx.x; e < L; e += blockDim.x) buf[e] = sm.A[e];
 }
 
 // per-level spectra of one instance in natural bin order
@@ -233,40 +243,6 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
 }
 
 // ---------------------------------------------------------------------- launch helpers
-template <class K>
-cudaError_t prep_kernel(K kern, const Plan &pl) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
-  if (e != cudaSuccess) return e;
-  if (pl.C > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return e;
-}
-
-template <class K, class... Args>
-cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Args... args) {
-  cudaError_t e = prep_kernel(kern, pl);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = size_t(pl.smem);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(pl.C);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
-template <int C>
-cudaError_t launch_solve_c(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) {
-  if (pl.method == TSF_BICGSTAB)
-    return launch_cluster(k_solve<C, TSF_BICGSTAB>, pl, pl.B * C, st, dp, nlev);
-  return launch_cluster(k_solve<C, TSF_CGNR>, pl, pl.B * C, st, dp, nlev);
-}
-
 cudaError_t launch_solve(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) {
   switch (pl.C) {
     case 1: return launch_solve_c<1>(pl, dp, nlev, st);
@@ -281,22 +257,22 @@ cudaError_t launch_solve(const Plan &pl, const DevParams &dp, int32_t nlev, cuda
 cudaError_t launch_dbg_apply(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
                              const double *in, double *out, cudaStream_t st) {
   switch (pl.C) {
-    case 1: return launch_cluster(k_debug_apply<1>, pl, 1, st, dp, b, j, which, in, out);
-    case 2: return launch_cluster(k_debug_apply<2>, pl, 2, st, dp, b, j, which, in, out);
-    case 4: return launch_cluster(k_debug_apply<4>, pl, 4, st, dp, b, j, which, in, out);
-    case 8: return launch_cluster(k_debug_apply<8>, pl, 8, st, dp, b, j, which, in, out);
-    case 16: return launch_cluster(k_debug_apply<16>, pl, 16, st, dp, b, j, which, in, out);
+    case 1: return launch_dbg_apply_c<1>(pl, dp, b, j, which, in, out, st);
+    case 2: return launch_dbg_apply_c<2>(pl, dp, b, j, which, in, out, st);
+    case 4: return launch_dbg_apply_c<4>(pl, dp, b, j, which, in, out, st);
+    case 8: return launch_dbg_apply_c<8>(pl, dp, b, j, which, in, out, st);
+    case 16: return launch_dbg_apply_c<16>(pl, dp, b, j, which, in, out, st);
   }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_dbg_rhs(const Plan &pl, const DevParams &dp, cudaStream_t st) {
   switch (pl.C) {
-    case 1: return launch_cluster(k_debug_rhs<1>, pl, pl.B, st, dp);
-    case 2: return launch_cluster(k_debug_rhs<2>, pl, pl.B * 2, st, dp);
-    case 4: return launch_cluster(k_debug_rhs<4>, pl, pl.B * 4, st, dp);
-    case 8: return launch_cluster(k_debug_rhs<8>, pl, pl.B * 8, st, dp);
-    case 16: return launch_cluster(k_debug_rhs<16>, pl, pl.B * 16, st, dp);
+    case 1: return launch_dbg_rhs_c<1>(pl, dp, st);
+    case 2: return launch_dbg_rhs_c<2>(pl, dp, st);
+    case 4: return launch_dbg_rhs_c<4>(pl, dp, st);
+    case 8: return launch_dbg_rhs_c<8>(pl, dp, st);
+    case 16: return launch_dbg_rhs_c<16>(pl, dp, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -636,8 +612,9 @@ int tsf_debug_local_fft(int64_t L, const double *x, double *y, int32_t inverse) 
   CK(cudaMalloc(&tw, size_t(2 * L) * 16));
   CK(cudaMemcpy(buf, x, size_t(L) * 16, cudaMemcpyHostToDevice));
   k_twiddle<<<grid_for(2 * L), 256>>>(tw, int(2 * L));
-  CK(cudaFuncSetAttribute(k_dbg_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L * 16)));
-  k_dbg_fft<<<1, kThreads, size_t(L) * 16>>>(buf, int(L), tw, int(2 * L), inverse);
+  const size_t dsm = size_t(L) * 16 + 16 * size_t(L / 64 + 64) + 1024;
+  CK(cudaFuncSetAttribute(k_dbg_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
+  k_dbg_fft<<<1, kThreads, dsm>>>(buf, int(L), tw, int(2 * L), inverse);
   CK(cudaGetLastError());
   CK(cudaMemcpy(y, buf, size_t(L) * 16, cudaMemcpyDeviceToHost));
   cudaFree(buf);
@@ -737,3 +714,12 @@ int tsf_debug_set_history(tsf_handle *h, int32_t inst, int64_t j, const double *
 }
 
 }  // extern "C"
+
+extern "C" int tsf_debug_prof(tsf_handle *h, uint64_t *out, int32_t reset) {
+  if (!h || !out) { set_error("bad arguments"); return TSF_E_ARG; }
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  CK(cudaMemcpy(out, h->dp.prof, 32 * 8, cudaMemcpyDeviceToHost));
+  if (reset) CK(cudaMemset(h->dp.prof, 0, 32 * 8));
+  return TSF_OK;
+}

@@ -1,21 +1,25 @@
 // tsf_kernels.cuh -- sm_100a FP64 device code of the per-level Toeplitz Krylov solver.
 //
-// One thread-block cluster of C CTAs owns one problem instance for a whole level (or for
-// the whole run).  Per level (alg1):
+// One thread-block cluster of C CTAs owns one problem instance for a whole run of levels.
+// Per level (alg1):
 //   RHS   g = B u^j - kappa sum_s c_{j-s} d^s + f^{j+sigma}          (eq3.1)
 //   Krylov solve A u^{j+1} = g, right-preconditioned BiCGSTAB or CGNR (CGLS on A P^{-1})
 //   finalize d^j = u^{j+1} - u^j (history), u^j <- u^{j+1}, per-level stats.
 // A, B are applied through the 2n circulant embedding of their Toeplitz generators (P:765-767,
-// P:775-776) and the preconditioner is a circulant solve; both are FFT
-// -> per-bin spectral op -> inverse FFT fused in shared memory:
-//   * the n real unknowns of a CTA are packed as n/(2C) complex values (real-FFT packing);
-//   * length-L complex transforms (L = n: embedding, L = n/2: preconditioner) use a
-//     four-step split L = C * L1: a local radix-4/2 FFT of length L1 per CTA in SMEM,
-//     a length-C DFT across the cluster through distributed shared memory, the per-bin
-//     real-split + spectral scaling in registers, and the transposed path back;
-//   * the per-level spectra are formed on the fly from one-time base spectra
-//     (lambda = eta + mu (c Lambda_Q + p Lambda_W + q conj Lambda_W)).
-// Reductions are deterministic (fixed-order warp shuffles, CTA, then cluster).
+// P:775-776) and the preconditioner is a circulant solve; each is
+// FFT -> per-bin spectral op -> inverse FFT, fused in shared memory:
+//   * the n real unknowns are packed as n/2 complex values z_m = x_{2m} + i x_{2m+1}
+//     (real-FFT packing); CTA r of the cluster owns z_m for m = r mod C;
+//   * a length-L complex transform (L = n: embedding, L = n/2: preconditioner) is a
+//     four-step split L = C x L1: an in-place radix-4/2 FFT of length L1 per CTA in SMEM
+//     (DIF forward into digit-reversed slots, DIT inverse back), a length-C DFT across the
+//     cluster through distributed shared memory, and the per-bin real split + spectral
+//     scaling on bin pairs (k, L-k) that the column-pair ownership keeps inside one CTA;
+//   * per-level spectra are formed on the fly from one-time base spectra:
+//     lambda = eta + mu (c Lambda_Q + p Lambda_W + q conj Lambda_W).
+// Krylov vectors live in registers when a CTA's chunk is small (VPT complex values per
+// thread and vector), else in global memory.  Reductions are deterministic (fixed-order warp
+// shuffles, CTA, cluster).
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -44,6 +48,7 @@ __device__ __forceinline__ double2 caxpy(double s, double2 x, double2 y) {  // y
   return make_double2(fma(s, x.x, y.x), fma(s, x.y, y.y));
 }
 __device__ __forceinline__ double cdot(double2 a, double2 b) { return a.x * b.x + a.y * b.y; }
+__device__ __forceinline__ double2 zero2() { return make_double2(0.0, 0.0); }
 
 // ------------------------------------------------------------------------ instance view
 struct Inst {
@@ -100,35 +105,101 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Deterministic cluster-wide sum of NV scalars: warp butterflies (exactly commutative, so
-// every lane holds the same bits) -> 8 warps in order -> C CTAs in rank order.
+// ------------------------------------------------------------------------ shared memory
+// [A: L1e][B: L1e if staged][thi: L1e/64][tlo: 64][wred: 40 doubles][cred: 8 doubles]
+struct Smem {
+  double2 *A, *B, *thi, *tlo;
+  double *wred, *cred;
+  unsigned long long *prof;
+};
+
+// Section timers (profiling build, -DTSF_PROFILE): thread 0 of block 0 accumulates clock64
+// cycles per section into P.prof[slot]; the wait at a barrier is charged to the section
+// that ends with it.
+#ifdef TSF_PROFILE
+#define TSF_PT0() long long tsf_pt_ = clock64()
+#define TSF_PACC(sm, slot)                                                                    \
+  do {                                                                                      \
+    const long long t_ = clock64();                                                         \
+    if (threadIdx.x == 0 && blockIdx.x == 0) (sm).prof[slot] += (unsigned long long)(t_ - tsf_pt_); \
+    tsf_pt_ = t_;                                                                           \
+  } while (0)
+#else
+#define TSF_PT0() do {} while (0)
+#define TSF_PACC(sm, slot) do {} while (0)
+#endif
+enum ProfSlot { PS_FFT_F = 0, PS_BAR1, PS_GATHER, PS_COLF, PS_PAIRS, PS_COLI, PS_BAR2, PS_SCATTER,
+                PS_BAR3, PS_FFT_I, PS_CSUM, PS_VEC, PS_RHS_HIST, PS_LEVEL, PS_APPLIES, PS_ITERS };
+__device__ __forceinline__ int tw_hi_len(int L1e) { return L1e >= 64 ? L1e / 64 : 1; }
+__device__ __forceinline__ int tw_lo_len(int L1e) { return L1e >= 64 ? 64 : L1e; }
+
+__device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, bool staged,
+                                          unsigned long long *prof) {
+  Smem s;
+  s.prof = prof;
+  s.A = reinterpret_cast<double2 *>(raw);
+  s.B = staged ? s.A + L1e : nullptr;
+  s.thi = s.A + L1e * (staged ? 2 : 1);
+  s.tlo = s.thi + tw_hi_len(L1e);
+  s.wred = reinterpret_cast<double *>(s.tlo + tw_lo_len(L1e));
+  s.cred = s.wred + 40;
+  return s;
+}
+
+// Two-level twiddle table of W_{L1e}: W^e = thi[e >> 6] * tlo[e & 63], copied from the
+// global table tw[x] = exp(-2 pi i x / twN).
+__device__ __forceinline__ void load_twiddles(const Smem &sm, int L1e, const double2 *tw, int twN) {
+  const int f = twN / L1e;
+  for (int i = threadIdx.x; i < tw_lo_len(L1e); i += kThreads) sm.tlo[i] = tw[i * f];
+  for (int i = threadIdx.x; i < tw_hi_len(L1e); i += kThreads) sm.thi[i] = tw[(i << 6) * f];
+}
+__device__ __forceinline__ double2 twid(const Smem &sm, int e) {
+  return cmul(sm.thi[e >> 6], sm.tlo[e & 63]);
+}
+
+// Deterministic cluster-wide sum of NV <= 4 scalars: warp butterflies (exactly commutative,
+// so every lane holds the same bits) -> 8 warps in order -> C CTA partials through a
+// 32-lane butterfly in warp 0 (lanes >= C add 0) -> broadcast.
 template <int C, int NV>
-__device__ __forceinline__ void csum(double (&v)[NV], double *wred, double *cred, int &par) {
+__device__ __forceinline__ void csum(double (&v)[NV], const Smem &sm, int &par) {
+  TSF_PT0();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) wred[warp * 4 + k] = v[k];
+    for (int k = 0; k < NV; ++k) sm.wred[warp * 4 + k] = v[k];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) s += wred[w * 4 + k];
-      cred[par * 4 + k] = s;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) s += sm.wred[w * 4 + k];
+      sm.cred[par * 4 + k] = s;
     }
   }
-  csync<C>();
+  if constexpr (C == 1) {
+    __syncthreads();
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = 0.0;
+    for (int k = 0; k < NV; ++k) v[k] = sm.cred[par * 4 + k];
+  } else {
+    csync<C>();
+    if (warp == 0) {
 #pragma unroll
-    for (int q = 0; q < C; ++q) s += remote<C>(cred, q)[par * 4 + k];
-    v[k] = s;
+      for (int k = 0; k < NV; ++k) {
+        double s = lane < C ? remote<C>(sm.cred, uint32_t(lane))[par * 4 + k] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) sm.wred[32 + k] = s;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = sm.wred[32 + k];
   }
   par ^= 1;
+  TSF_PACC(sm, PS_CSUM);
 }
 
 // ------------------------------------------------------------------------ local FFT (SMEM)
@@ -136,8 +207,7 @@ __device__ __forceinline__ void csum(double (&v)[NV], double *wred, double *cred
 // radix 2 when l = log2(L1) is odd; m_s = prod_{t<=s} r_t.  The forward transform runs the
 // transposed stages (DIF, S-1..0) in place: natural input -> slot order, slot p holding
 // X[perm[p]] with perm the gather digit reversal.  The inverse runs the conjugated DIT stages
-// 0..S-1 in place: slot order -> natural order (unnormalized).  Twiddles W_m^{kq} come from
-// the table tw[e] = exp(-2 pi i e / twN).
+// 0..S-1 in place: slot order -> natural order (unnormalized).
 template <bool INV>
 __device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, double2 &a3) {
   const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3);
@@ -149,21 +219,20 @@ __device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, dou
   a3 = csub(t1, t3);
 }
 
-template <bool INV>
-__device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, int radix,
-                                          const double2 *__restrict__ tw, int twN) {
-  // lm = log2(m_s); radix 4 or 2; mprev = m_s / radix
-  const int lmp = lm - (radix == 4 ? 2 : 1);
+// one stage: m = 2^lm, twiddle W_m^{kq} = W_{L1e}^{kq (L1e/m)}
+template <bool INV, int RADIX>
+__device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem &sm, int L1e) {
+  const int lmp = lm - (RADIX == 4 ? 2 : 1);
   const int mprev = 1 << lmp;
-  const int tstep = twN >> lm;                 // W_m^x = tw[x * twN/m]
-  const int nb = L1 / radix;
+  const int tstep = L1e >> lm;
+  const int nb = L1 / RADIX;
   for (int b = threadIdx.x; b < nb; b += kThreads) {
     const int k = b & (mprev - 1);
     const int base = ((b >> lmp) << lm) + k;
-    if (radix == 4) {
+    if constexpr (RADIX == 4) {
       double2 a0 = A[base], a1 = A[base + mprev], a2 = A[base + 2 * mprev], a3 = A[base + 3 * mprev];
       if (k != 0) {
-        const double2 w1 = tw[k * tstep], w2 = tw[2 * k * tstep], w3 = tw[3 * k * tstep];
+        const double2 w1 = twid(sm, k * tstep), w2 = twid(sm, 2 * k * tstep), w3 = twid(sm, 3 * k * tstep);
         if (INV) {
           a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
           bfly4<true>(a0, a1, a2, a3);
@@ -177,7 +246,7 @@ __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, int radix,
       A[base] = a0; A[base + mprev] = a1; A[base + 2 * mprev] = a2; A[base + 3 * mprev] = a3;
     } else {
       double2 a0 = A[base], a1 = A[base + mprev];
-      const double2 w = tw[k * tstep];
+      const double2 w = twid(sm, k * tstep);
       if (INV) {
         a1 = cmulc(a1, w);
         A[base] = cadd(a0, a1); A[base + mprev] = csub(a0, a1);
@@ -190,21 +259,21 @@ __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, int radix,
 
 // Requires the input to be visible to all threads (caller synchronizes); ends synchronized.
 template <bool INV>
-__device__ __noinline__ void local_fft(double2 *A, int L1, const double2 *__restrict__ tw, int twN) {
+__device__ __noinline__ void local_fft(double2 *A, int L1, const Smem &sm, int L1e) {
   const int l = __ffs(L1) - 1;
   const int S4 = l >> 1;
   const bool r2 = l & 1;
   const int S = S4 + (r2 ? 1 : 0);
   if (!INV) {
     for (int s = S - 1; s >= 0; --s) {
-      if (r2 && s == S - 1) fft_stage<false>(A, L1, l, 2, tw, twN);
-      else fft_stage<false>(A, L1, 2 * (s + 1), 4, tw, twN);
+      if (r2 && s == S - 1) fft_stage<false, 2>(A, L1, l, sm, L1e);
+      else fft_stage<false, 4>(A, L1, 2 * (s + 1), sm, L1e);
       __syncthreads();
     }
   } else {
     for (int s = 0; s < S; ++s) {
-      if (r2 && s == S - 1) fft_stage<true>(A, L1, l, 2, tw, twN);
-      else fft_stage<true>(A, L1, 2 * (s + 1), 4, tw, twN);
+      if (r2 && s == S - 1) fft_stage<true, 2>(A, L1, l, sm, L1e);
+      else fft_stage<true, 4>(A, L1, 2 * (s + 1), sm, L1e);
       __syncthreads();
     }
   }
@@ -325,7 +394,7 @@ struct Geo {
 // C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).
 template <bool DIV>
 __device__ __noinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
-                                                const double2 *__restrict__ tw) {
+                                             const double2 *__restrict__ tw) {
   for (int i = threadIdx.x; i < g.np; i += kThreads) {
     if (i == 0) {
       const int sa = g.slot[0], sb = g.slot[g.L1 / 2];
@@ -343,11 +412,121 @@ __device__ __noinline__ void pointwise_local(double2 *A, const Geo &g, const Spe
   }
 }
 
-// C > 1: gather the C partial transforms of column pair (k1a, k1b) through DSMEM, finish the
-// four-step transform with a length-C DFT, apply the spectral op, undo, scatter back.
+// column pair i of CTA r: (k1a, k1b) = (pi, L1 - pi) with pi = r + i C, or (0, L1/2) for pi = 0
+__device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col) {
+  const int pi = int(r) + (col >> 1) * C;
+  if (pi == 0) return (col & 1) ? L1 / 2 : 0;
+  return (col & 1) ? L1 - pi : pi;
+}
+
+// C > 1, staged through the local buffer B (layout B[q * ncol + col], ncol = L1/C):
+//   gather A_q[slot(k1)] from every CTA -> per column: twiddle W_L^{q k1}, DFT_C -> per bin
+//   pair: spectral op -> per column: inverse DFT_C, conj twiddle -> scatter to A_{m2}.
 template <int C, bool DIV>
-__device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &op,
-                                           const double2 *__restrict__ tw, uint32_t r) {
+__device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, const SpecOp &op,
+                                          const double2 *__restrict__ tw, uint32_t r, const Smem &sm) {
+  TSF_PT0();
+  const int ncol = g.L1 / C;
+  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM gather
+    const int q = u / ncol, col = u - q * ncol;
+    B[u] = remote<C>(A, uint32_t(q))[g.slot[col_k1(g.L1, C, r, col)]];
+  }
+  __syncthreads();
+  TSF_PACC(sm, PS_GATHER);
+  for (int col = threadIdx.x; col < ncol; col += kThreads) {  // column DFT_C
+    const int k1 = col_k1(g.L1, C, r, col);
+    double2 z[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
+#pragma unroll
+    for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+    fft_reg<C, false>(z);
+#pragma unroll
+    for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
+  }
+  __syncthreads();
+  TSF_PACC(sm, PS_COLF);
+  // bin pairs: item u = k2 * np + i; regular pair (col 2i row k2) <-> (col 2i+1 row C-1-k2)
+  for (int u = threadIdx.x; u < g.np * C; u += kThreads) {
+    const int k2 = u / g.np, i = u - k2 * g.np;
+    const int pi = int(r) + i * C;
+    if (pi != 0) {
+      const int bin = pi + g.L1 * k2;
+      double2 &za = B[k2 * ncol + 2 * i];
+      double2 &zb = B[(C - 1 - k2) * ncol + 2 * i + 1];
+      double2 a = za, b = zb;
+      pair_apply<DIV>(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
+                      tw[bin * g.tw2L], op.scale);
+      za = a;
+      zb = b;
+    } else {
+      // column 0 (bins L1 k2) pairs k2 <-> (C - k2) mod C; k2 = 0 pairs with the Nyquist bin
+      const int kk = (C - k2) % C;
+      if (k2 <= C / 2) {
+        const int bin = g.L1 * k2;
+        const double2 la = op.get(k2, 0, 0, bin);
+        double2 &za = B[k2 * ncol];
+        if (kk == k2) {
+          double2 a = za;
+          pair_self<DIV>(a, la, k2 == 0 ? op.nyquist(g.L) : la, tw[bin * g.tw2L], op.scale);
+          za = a;
+        } else {
+          double2 &zb = B[kk * ncol];
+          double2 a = za, b = zb;
+          pair_apply<DIV>(a, b, la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+          za = a;
+          zb = b;
+        }
+      }
+      // column L1/2 (bins L1/2 + L1 k2) pairs k2 <-> C-1-k2
+      const int km = C - 1 - k2;
+      if (k2 < (C + 1) / 2) {
+        const int bin = g.L1 / 2 + g.L1 * k2;
+        const double2 la = op.get(k2, 1, 0, bin);
+        double2 &za = B[k2 * ncol + 1];
+        if (km == k2) {
+          double2 a = za;
+          pair_self<DIV>(a, la, la, tw[bin * g.tw2L], op.scale);
+          za = a;
+        } else {
+          double2 &zb = B[km * ncol + 1];
+          double2 a = za, b = zb;
+          pair_apply<DIV>(a, b, la, op.get(km, 1, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+          za = a;
+          zb = b;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  TSF_PACC(sm, PS_PAIRS);
+  for (int col = threadIdx.x; col < ncol; col += kThreads) {  // inverse column DFT_C
+    const int k1 = col_k1(g.L1, C, r, col);
+    double2 z[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
+    fft_reg<C, true>(z);
+#pragma unroll
+    for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+#pragma unroll
+    for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
+  }
+  TSF_PACC(sm, PS_COLI);
+  csync<C>();                    // every gather of A done before any scatter overwrites it
+  TSF_PACC(sm, PS_BAR2);
+  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM scatter
+    const int q = u / ncol, col = u - q * ncol;
+    remote<C>(A, uint32_t(q))[g.slot[col_k1(g.L1, C, r, col)]] = B[u];
+  }
+  TSF_PACC(sm, PS_SCATTER);
+  csync<C>();                    // scatters landed
+}
+
+// C > 1 without a staging buffer (shared memory full): one thread per column pair keeps the
+// 2C values in registers across the barrier.  Requires np <= kThreads.
+template <int C, bool DIV>
+__device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &op,
+                                       const double2 *__restrict__ tw, uint32_t r) {
   double2 za[C], zb[C];
   const int i = threadIdx.x;
   const bool act = i < g.np;
@@ -372,7 +551,6 @@ __device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &
     }
     fft_reg<C, false>(za);
     fft_reg<C, false>(zb);
-    // za[k2] = Z[k1a + L1 k2], zb[k2] = Z[k1b + L1 k2]
     if (!pseudo) {
 #pragma unroll
       for (int k2 = 0; k2 < C; ++k2) {
@@ -381,7 +559,6 @@ __device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &
                         op.get(C - 1 - k2, 1, i, g.L - bin), tw[bin * g.tw2L], op.scale);
       }
     } else {
-      // column 0: bins L1 k2 paired with L1 (C - k2) (k2 = 0 pairs with the Nyquist bin)
 #pragma unroll
       for (int k2 = 0; k2 <= C / 2; ++k2) {
         const int kk = (C - k2) % C;
@@ -394,7 +571,6 @@ __device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &
           pair_apply<DIV>(za[k2], za[kk], la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
         }
       }
-      // column L1/2: bins L1/2 + L1 k2 paired with L1/2 + L1 (C-1-k2)
 #pragma unroll
       for (int k2 = 0; k2 < (C + 1) / 2; ++k2) {
         const int kk = C - 1 - k2;
@@ -412,7 +588,7 @@ __device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &
       zb[q] = cmulc(zb[q], tw[q * k1b * g.twL]);
     }
   }
-  csync<C>();                    // every gather done before any scatter overwrites
+  csync<C>();
   if (act) {
 #pragma unroll
     for (int q = 0; q < C; ++q) {
@@ -421,23 +597,33 @@ __device__ __noinline__ void cross_step(double2 *A, const Geo &g, const SpecOp &
       Aq[sb] = zb[q];
     }
   }
-  csync<C>();                    // scatters landed
+  csync<C>();
 }
 
 // y = op(x) for the CTA's local data already in A[0..L1) (natural order, visible).
 // On return A[0..L1) holds this CTA's part of the result (natural order, visible).
 template <int C, bool DIV>
-__device__ __noinline__ void apply(double2 *A, const Geo &g, const SpecOp &op,
-                                      const double2 *__restrict__ tw, int twN, uint32_t r) {
-  local_fft<false>(A, g.L1, tw, twN);
+__device__ __noinline__ void apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                   const double2 *__restrict__ tw, uint32_t r) {
+  TSF_PT0();
+  local_fft<false>(sm.A, g.L1, sm, L1e);
+  TSF_PACC(sm, PS_FFT_F);
   if constexpr (C == 1) {
-    pointwise_local<DIV>(A, g, op, tw);
+    pointwise_local<DIV>(sm.A, g, op, tw);
     __syncthreads();
+    TSF_PACC(sm, PS_PAIRS);
   } else {
     csync<C>();                  // every local transform done before remote gathers
-    cross_step<C, DIV>(A, g, op, tw, r);
+    TSF_PACC(sm, PS_BAR1);
+    if (sm.B) cross_staged<C, DIV>(sm.A, sm.B, g, op, tw, r, sm);
+    else cross_reg<C, DIV>(sm.A, g, op, tw, r);
+    TSF_PACC(sm, PS_BAR3);
   }
-  local_fft<true>(A, g.L1, tw, twN);
+  local_fft<true>(sm.A, g.L1, sm, L1e);
+  TSF_PACC(sm, PS_FFT_I);
+#ifdef TSF_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x == 0) sm.prof[PS_APPLIES] += 1;
+#endif
 }
 
 // ------------------------------------------------------------------------ operator setup
@@ -487,48 +673,61 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
   return op;
 }
 
-// ------------------------------------------------------------------------ shared memory
-struct Smem {
-  double2 *A;
-  double *wred, *cred;
+// ------------------------------------------------------------------------ vector storage
+// VPT > 0: this thread's VPT complex elements e = tid + q T in registers; VPT == 0: global.
+template <int VPT>
+struct VecT {
+  double2 d[VPT > 0 ? VPT : 1];
+  double2 *p;
+  __device__ __forceinline__ double2 &operator()(int q, int e) {
+    if constexpr (VPT > 0) return d[q];
+    else return p[e];
+  }
 };
-__device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e) {
-  Smem s;
-  s.A = reinterpret_cast<double2 *>(raw);
-  s.wred = reinterpret_cast<double *>(s.A + L1e);
-  s.cred = s.wred + 32;
-  return s;
+
+template <int VPT, class F>
+__device__ __forceinline__ void for_elems(int npc, F &&f) {
+  if constexpr (VPT > 0) {
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int e = threadIdx.x + q * kThreads;
+      if (e < npc) f(q, e);
+    }
+  } else {
+    for (int e = threadIdx.x; e < npc; e += kThreads) f(0, e);
+  }
+}
+
+template <int VPT>
+__device__ __forceinline__ void bind(VecT<VPT> &v, double *base, int64_t n, int slot, int off) {
+  v.p = reinterpret_cast<double2 *>(base + slot * n) + off;
 }
 
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
-// writes g to R (and RH, P for BiCGSTAB), zeroes X; returns the local partial ||g||^2.
-template <int C>
-__device__ __noinline__ double rhs_phase(const DevParams &P, const Inst &I, int64_t j, const Smem &sm, uint32_t r,
-                            bool bicg) {
+// Returns the local partial ||g||^2; g is left in A[0..npc) (and A[npc..2npc) is zero).
+template <int C, int VPT>
+__device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
+                                            uint32_t r, VecT<VPT> &U) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  double2 *U = reinterpret_cast<double2 *>(I.vec + V_U * n) + r * npc;
-  for (int e = threadIdx.x; e < npc; e += kThreads) {
-    sm.A[e] = U[e];
-    sm.A[e + npc] = make_double2(0.0, 0.0);
-  }
+  for_elems<VPT>(npc, [&](int q, int e) {
+    sm.A[e] = U(q, e);
+    sm.A[e + npc] = zero2();
+  });
   __syncthreads();
   const SpecOp opB = make_op(P, I, j, OP_B, r);
-  apply<C, false>(sm.A, geo_embed(P), opB, tw, P.twN, r);
-  double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * n) + r * npc;
-  double2 *RH = reinterpret_cast<double2 *>(I.vec + V_RH * n) + r * npc;
-  double2 *PV = reinterpret_cast<double2 *>(I.vec + V_P * n) + r * npc;
-  double2 *X = reinterpret_cast<double2 *>(I.vec + V_X * n) + r * npc;
+  apply<C, false>(sm, P.L1e, geo_embed(P), opB, tw, r);
   const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
   const int64_t hstride = n / 2;  // double2 per history row
   double acc = 0.0;
-  for (int e = threadIdx.x; e < npc; e += kThreads) {
+  TSF_PT0();
+  for_elems<VPT>(npc, [&](int, int e) {
     double2 g = sm.A[e];
     if (j >= 1) {
       double2 h0 = cscale(H[e], I.hwe[j]);
-      double2 h1 = make_double2(0.0, 0.0), h2 = h1, h3 = h1;
+      double2 h1 = zero2(), h2 = h1, h3 = h1;
       int64_t s = 1;
       for (; s + 3 <= j - 1; s += 4) {
         const double2 d0 = H[s * hstride + e], d1 = H[(s + 1) * hstride + e];
@@ -548,30 +747,44 @@ __device__ __noinline__ double rhs_phase(const DevParams &P, const Inst &I, int6
       const double2 *F = reinterpret_cast<const double2 *>(I.ftab) + r * npc;
       g = cadd(g, F[j * hstride + e]);
     }
-    R[e] = g;
-    if (bicg) { RH[e] = g; PV[e] = g; }
-    X[e] = make_double2(0.0, 0.0);
+    sm.A[e] = g;
+    sm.A[e + npc] = zero2();
     acc += cdot(g, g);
-  }
+  });
+  TSF_PACC(sm, PS_RHS_HIST);
   return acc;
 }
 
 // ------------------------------------------------------------------------ one level
-// Returns through the stats arrays; all control flow is uniform over the cluster.
-template <int C, int METHOD>
-__device__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const Smem &sm, uint32_t r) {
+// All control flow is uniform over the cluster (every CTA reduces to identical scalars).
+template <int C, int METHOD, int VPT>
+__device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
+                                            uint32_t r, VecT<VPT> &U) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  auto vec = [&](int v) { return reinterpret_cast<double2 *>(I.vec + v * n) + r * npc; };
-  double2 *X = vec(V_X), *R = vec(V_R), *RH = vec(V_RH), *PV = vec(V_P), *VV = vec(V_V);
-  double2 *S = vec(V_S), *PH = vec(V_PH), *SH = vec(V_SH);
   const bool prec = P.precond != TSF_NOPREC;
   const Geo ge = geo_embed(P), gp = geo_prec(P);
+  VecT<VPT> X, R, RH, PV, VV, S, PH, SH;
+  if constexpr (VPT == 0) {
+    const int off = int(r) * npc;
+    bind(X, I.vec, n, V_X, off); bind(R, I.vec, n, V_R, off); bind(RH, I.vec, n, V_RH, off);
+    bind(PV, I.vec, n, V_P, off); bind(VV, I.vec, n, V_V, off); bind(S, I.vec, n, V_S, off);
+    bind(PH, I.vec, n, V_PH, off); bind(SH, I.vec, n, V_SH, off);
+  }
   int par = 0;
+#ifdef TSF_PROFILE
+  const long long tlev0 = clock64();
+#endif
 
-  double g2[1] = {rhs_phase<C>(P, I, j, sm, r, METHOD == TSF_BICGSTAB)};
-  csum<C, 1>(g2, sm.wred, sm.cred, par);
+  double g2[1] = {rhs_phase<C, VPT>(P, I, j, sm, r, U)};
+  for_elems<VPT>(npc, [&](int q, int e) {
+    const double2 g = sm.A[e];
+    R(q, e) = g;
+    if (METHOD == TSF_BICGSTAB) { RH(q, e) = g; PV(q, e) = g; }
+    X(q, e) = zero2();
+  });
+  csum<C, 1>(g2, sm, par);
   const double rr0 = g2[0];
   const double rn0 = sqrt(rr0);
   int hs = 0, status = TSF_LEVEL_OK;
@@ -583,75 +796,75 @@ __device__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const 
     double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
     for (int it = 0;; ++it) {
       // Phase A: p = r + beta (p - omega v); phat = P^{-1} p; v = A phat; r^.v
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
+      for_elems<VPT>(npc, [&](int q, int e) {
         double2 pv;
-        if (it == 0) pv = R[e];
+        if (it == 0) pv = R(q, e);
         else {
-          pv = caxpy(beta, caxpy(-omega, VV[e], PV[e]), R[e]);
-          PV[e] = pv;
+          pv = caxpy(beta, caxpy(-omega, VV(q, e), PV(q, e)), R(q, e));
+          PV(q, e) = pv;
         }
         sm.A[e] = pv;
-      }
+      });
       __syncthreads();
-      if (prec) apply<C, true>(sm.A, gp, opP, tw, P.twN, r);
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        PH[e] = sm.A[e];
-        sm.A[e + npc] = make_double2(0.0, 0.0);
-      }
+      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      for_elems<VPT>(npc, [&](int q, int e) {
+        PH(q, e) = sm.A[e];
+        sm.A[e + npc] = zero2();
+      });
       __syncthreads();
-      apply<C, false>(sm.A, ge, opA, tw, P.twN, r);
+      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
       double d[1] = {0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
+      for_elems<VPT>(npc, [&](int q, int e) {
         const double2 v = sm.A[e];
-        VV[e] = v;
-        d[0] += cdot(RH[e], v);
-      }
-      csum<C, 1>(d, sm.wred, sm.cred, par);
+        VV(q, e) = v;
+        d[0] += cdot(RH(q, e), v);
+      });
+      csum<C, 1>(d, sm, par);
       if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       alpha = rho / d[0];
       // Phase B: s = r - alpha v; half-step exit on ||s||
       double ss[1] = {0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        const double2 s = caxpy(-alpha, sm.A[e], R[e]);
-        S[e] = s;
+      for_elems<VPT>(npc, [&](int q, int e) {
+        const double2 s = caxpy(-alpha, VV(q, e), R(q, e));
+        S(q, e) = s;
         sm.A[e] = s;
         ss[0] += cdot(s, s);
-      }
-      csum<C, 1>(ss, sm.wred, sm.cred, par);
+      });
+      csum<C, 1>(ss, sm, par);
       if (sqrt(ss[0]) < P.tol * rn0) {
-        for (int e = threadIdx.x; e < npc; e += kThreads) X[e] = caxpy(alpha, PH[e], X[e]);
+        for_elems<VPT>(npc, [&](int q, int e) { X(q, e) = caxpy(alpha, PH(q, e), X(q, e)); });
         hs += 1;
         relres = sqrt(ss[0]) / rn0;
         break;
       }
       //          shat = P^{-1} s; t = A shat; t.s, t.t
-      if (prec) apply<C, true>(sm.A, gp, opP, tw, P.twN, r);
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        SH[e] = sm.A[e];
-        sm.A[e + npc] = make_double2(0.0, 0.0);
-      }
+      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      for_elems<VPT>(npc, [&](int q, int e) {
+        SH(q, e) = sm.A[e];
+        sm.A[e + npc] = zero2();
+      });
       __syncthreads();
-      apply<C, false>(sm.A, ge, opA, tw, P.twN, r);
+      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
       double tt[2] = {0.0, 0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
+      for_elems<VPT>(npc, [&](int q, int e) {
         const double2 t = sm.A[e];
-        const double2 s = S[e];
+        const double2 s = S(q, e);
         tt[0] += cdot(t, s);
         tt[1] += cdot(t, t);
-      }
-      csum<C, 2>(tt, sm.wred, sm.cred, par);
+      });
+      csum<C, 2>(tt, sm, par);
       if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       omega = tt[0] / tt[1];
       // Phase C: x += alpha phat + omega shat; r = s - omega t; r^.r, r.r
       double rr[2] = {0.0, 0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        X[e] = caxpy(omega, SH[e], caxpy(alpha, PH[e], X[e]));
-        const double2 rn = caxpy(-omega, sm.A[e], S[e]);
-        R[e] = rn;
-        rr[0] += cdot(RH[e], rn);
+      for_elems<VPT>(npc, [&](int q, int e) {
+        X(q, e) = caxpy(omega, SH(q, e), caxpy(alpha, PH(q, e), X(q, e)));
+        const double2 rn = caxpy(-omega, sm.A[e], S(q, e));
+        R(q, e) = rn;
+        rr[0] += cdot(RH(q, e), rn);
         rr[1] += cdot(rn, rn);
-      }
-      csum<C, 2>(rr, sm.wred, sm.cred, par);
+      });
+      csum<C, 2>(rr, sm, par);
       hs += 2;
       relres = sqrt(rr[1]) / rn0;
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
@@ -665,114 +878,116 @@ __device__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const 
     // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r, p = z.
     const SpecOp opAT = make_op(P, I, j, OP_AT, r);
     const SpecOp opPT = make_op(P, I, j, OP_PTINV, r);
-    double2 *Q = VV;
-    for (int e = threadIdx.x; e < npc; e += kThreads) {
-      sm.A[e] = R[e];
-      sm.A[e + npc] = make_double2(0.0, 0.0);
-    }
+    // A[0..npc) holds r = g and A[npc..) is zero (rhs_phase)
     __syncthreads();
-    apply<C, false>(sm.A, ge, opAT, tw, P.twN, r);
-    if (prec) apply<C, true>(sm.A, gp, opPT, tw, P.twN, r);
+    apply<C, false>(sm, P.L1e, ge, opAT, tw, r);
+    if (prec) apply<C, true>(sm, P.L1e, gp, opPT, tw, r);
     double gz[1] = {0.0};
-    for (int e = threadIdx.x; e < npc; e += kThreads) {
+    for_elems<VPT>(npc, [&](int q, int e) {
       const double2 z = sm.A[e];
-      PV[e] = z;
+      PV(q, e) = z;
       gz[0] += cdot(z, z);
-    }
-    csum<C, 1>(gz, sm.wred, sm.cred, par);
+    });
+    csum<C, 1>(gz, sm, par);
     double gam = gz[0];
     double beta = 0.0;
     for (int it = 0;; ++it) {
       // Phase A: p = z + beta p; phat = P^{-1} p; q = A phat; ||q||^2
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
+      for_elems<VPT>(npc, [&](int q, int e) {
         double2 pv;
-        if (it == 0) pv = PV[e];
-        else { pv = caxpy(beta, PV[e], sm.A[e]); PV[e] = pv; }
+        if (it == 0) pv = PV(q, e);
+        else { pv = caxpy(beta, PV(q, e), sm.A[e]); PV(q, e) = pv; }
         sm.A[e] = pv;
-      }
+      });
       __syncthreads();
-      if (prec) apply<C, true>(sm.A, gp, opP, tw, P.twN, r);
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        PH[e] = sm.A[e];
-        sm.A[e + npc] = make_double2(0.0, 0.0);
-      }
+      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      for_elems<VPT>(npc, [&](int q, int e) {
+        PH(q, e) = sm.A[e];
+        sm.A[e + npc] = zero2();
+      });
       __syncthreads();
-      apply<C, false>(sm.A, ge, opA, tw, P.twN, r);
+      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
       double qq[1] = {0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        const double2 q = sm.A[e];
-        Q[e] = q;
-        qq[0] += cdot(q, q);
-      }
-      csum<C, 1>(qq, sm.wred, sm.cred, par);
+      for_elems<VPT>(npc, [&](int, int e) { qq[0] += cdot(sm.A[e], sm.A[e]); });
+      csum<C, 1>(qq, sm, par);
       if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       const double a = gam / qq[0];
       // Phase B: x += a phat; r -= a q; ||r||; z = P^{-T} A^T r; ||z||^2
       double rl[1] = {0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) {
-        X[e] = caxpy(a, PH[e], X[e]);
-        const double2 rn = caxpy(-a, sm.A[e], R[e]);
-        R[e] = rn;
+      for_elems<VPT>(npc, [&](int q, int e) {
+        X(q, e) = caxpy(a, PH(q, e), X(q, e));
+        const double2 rn = caxpy(-a, sm.A[e], R(q, e));
+        R(q, e) = rn;
         sm.A[e] = rn;
-        sm.A[e + npc] = make_double2(0.0, 0.0);
+        sm.A[e + npc] = zero2();
         rl[0] += cdot(rn, rn);
-      }
-      csum<C, 1>(rl, sm.wred, sm.cred, par);
+      });
+      csum<C, 1>(rl, sm, par);
       hs += 2;
       relres = sqrt(rl[0] / rr0);
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
       if (relres < P.tol) break;
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
-      apply<C, false>(sm.A, ge, opAT, tw, P.twN, r);
-      if (prec) apply<C, true>(sm.A, gp, opPT, tw, P.twN, r);
+      apply<C, false>(sm, P.L1e, ge, opAT, tw, r);
+      if (prec) apply<C, true>(sm, P.L1e, gp, opPT, tw, r);
       double zz[1] = {0.0};
-      for (int e = threadIdx.x; e < npc; e += kThreads) zz[0] += cdot(sm.A[e], sm.A[e]);
-      csum<C, 1>(zz, sm.wred, sm.cred, par);
+      for_elems<VPT>(npc, [&](int, int e) { zz[0] += cdot(sm.A[e], sm.A[e]); });
+      csum<C, 1>(zz, sm, par);
       beta = zz[0] / gam;
       gam = zz[0];
     }
   }
   // finalize (alg1 step 3 result): d^j = u^{j+1} - u^j, u^j <- u^{j+1}
-  double2 *U = vec(V_U);
   double2 *Hj = reinterpret_cast<double2 *>(I.hist + j * n) + r * npc;
-  for (int e = threadIdx.x; e < npc; e += kThreads) {
-    const double2 x = X[e], u = U[e];
+  for_elems<VPT>(npc, [&](int q, int e) {
+    const double2 x = X(q, e), u = U(q, e);
     Hj[e] = csub(x, u);
-    U[e] = x;
-  }
+    U(q, e) = x;
+  });
   if (r == 0 && threadIdx.x == 0) {
     I.it[j] = hs;
     I.rr[j] = relres;
     I.st[j] = status;
   }
   __syncthreads();
+#ifdef TSF_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    sm.prof[PS_LEVEL] += (unsigned long long)(clock64() - tlev0);
+    sm.prof[PS_ITERS] += (unsigned long long)hs;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------ kernels
-template <int C, int METHOD>
-__global__ void __launch_bounds__(kThreads, 1) k_solve(DevParams P, int32_t nlev) {
+template <int C, int METHOD, int VPT>
+__global__ void __launch_bounds__(kThreads, (C == 1 && VPT == 0) ? 2 : 1)
+    k_solve(DevParams P, int32_t nlev, int32_t staged) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e);
+  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
+  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+  const int npc = P.L1p;
+  VecT<VPT> U;
+  double2 *Ug = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
+  if constexpr (VPT > 0) for_elems<VPT>(npc, [&](int q, int e) { U(q, e) = Ug[e]; });
+  else U.p = Ug;
+  __syncthreads();
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD>(P, I, j, sm, r);
+  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, VPT>(P, I, j, sm, r, U);
+  if constexpr (VPT > 0) for_elems<VPT>(npc, [&](int q, int e) { Ug[e] = U(q, e); });
 }
 
-__global__ void k_advance(int64_t *level, int64_t by, int64_t M) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    const int64_t v = *level + by;
-    *level = v < M ? v : M;
-  }
-}
+__global__ void k_advance(int64_t *level, int64_t by, int64_t M);
 
 // Debug: one operator application of instance b at level j: in/out are permuted chunks.
 template <int C>
-__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int b, int64_t j, int which,
-                                                              const double *in, double *out) {
+__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t staged, int b, int64_t j,
+                                                              int which, const double *in, double *out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e);
+  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
+  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
   const int npc = P.L1p;
@@ -782,25 +997,91 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int b,
   const bool embed = which <= OP_AT;
   for (int e = threadIdx.x; e < npc; e += kThreads) {
     sm.A[e] = X[e];
-    if (embed) sm.A[e + npc] = make_double2(0.0, 0.0);
+    if (embed) sm.A[e + npc] = zero2();
   }
   __syncthreads();
   const SpecOp op = make_op(P, I, j, which, r);
-  if (embed) apply<C, false>(sm.A, geo_embed(P), op, tw, P.twN, r);
-  else apply<C, true>(sm.A, geo_prec(P), op, tw, P.twN, r);
+  if (embed) apply<C, false>(sm, P.L1e, geo_embed(P), op, tw, r);
+  else apply<C, true>(sm, P.L1e, geo_prec(P), op, tw, r);
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = sm.A[e];
 }
 
 // Debug: RHS of the current level for every instance into V_R.
 template <int C>
-__global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P) {
+__global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t staged) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e);
+  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
+  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
   const int64_t j = *P.level;
-  if (j < P.M) rhs_phase<C>(P, I, j, sm, r, false);
+  const int npc = P.L1p;
+  __syncthreads();
+  if (j >= P.M) return;
+  VecT<0> U;
+  U.p = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
+  rhs_phase<C, 0>(P, I, j, sm, r, U);
+  double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
+  for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[e];
 }
+
+// ------------------------------------------------------------------------ launch API
+// Implemented per cluster size in tsf_solve_c<C>.cu (parallel compilation).
+template <int C>
+cudaError_t launch_solve_c(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st);
+template <int C>
+cudaError_t launch_dbg_apply_c(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
+                               const double *in, double *out, cudaStream_t st);
+template <int C>
+cudaError_t launch_dbg_rhs_c(const Plan &pl, const DevParams &dp, cudaStream_t st);
+
+// Cluster launch with the plan's dynamic shared memory.
+template <class K, class... Args>
+cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Args... args) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+  if (e != cudaSuccess) return e;
+  if (pl.C > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = size_t(pl.smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(pl.C);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+#define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
+  template <>                                                                                   \
+  cudaError_t launch_solve_c<CC>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) { \
+    const int g = pl.B * CC;                                                                    \
+    const int32_t stg = pl.staged;                                                              \
+    if (pl.method == TSF_BICGSTAB) {                                                            \
+      if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 1>, pl, g, st, dp, nlev, stg); \
+      if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 2>, pl, g, st, dp, nlev, stg); \
+      return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0>, pl, g, st, dp, nlev, stg);            \
+    }                                                                                           \
+    if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_CGNR, 1>, pl, g, st, dp, nlev, stg); \
+    if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_CGNR, 2>, pl, g, st, dp, nlev, stg); \
+    return launch_cluster(k_solve<CC, TSF_CGNR, 0>, pl, g, st, dp, nlev, stg);                  \
+  }                                                                                             \
+  template <>                                                                                   \
+  cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \
+                                     int which, const double *in, double *out, cudaStream_t st) { \
+    return launch_cluster(k_debug_apply<CC>, pl, CC, st, dp, int32_t(pl.staged), b, j, which, in, out); \
+  }                                                                                             \
+  template <>                                                                                   \
+  cudaError_t launch_dbg_rhs_c<CC>(const Plan &pl, const DevParams &dp, cudaStream_t st) {      \
+    return launch_cluster(k_debug_rhs<CC>, pl, pl.B * CC, st, dp, int32_t(pl.staged));          \
+  }
 
 }  // namespace tsf

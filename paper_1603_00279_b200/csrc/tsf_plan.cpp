@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace tsf {
@@ -139,7 +140,15 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.L1p = int32_t(n / (2 * C));
   P.npe = P.L1e / (2 * C);
   P.npp = P.L1p / (2 * C);
-  P.smem = int64_t(16) * P.L1e + 1024;
+  // Krylov vectors in registers when a CTA's chunk is at most 2 complex values per thread
+  const int64_t npc = n / (2 * C);
+  P.vpt = npc <= kThreads ? 1 : (npc <= 2 * kThreads ? 2 : 0);
+  if (const char *ev = std::getenv("TSF_VPT")) P.vpt = std::atoi(ev);
+  // staged cross-CTA exchange when two local buffers fit (L1e <= 4096)
+  P.staged = (C > 1 && P.L1e <= 4096) ? 1 : 0;
+  if (const char *es = std::getenv("TSF_STAGED")) P.staged = (C > 1) ? std::atoi(es) : 0;
+  const int64_t thi = P.L1e >= 64 ? P.L1e / 64 : 1, tlo = P.L1e >= 64 ? 64 : P.L1e;
+  P.smem = int64_t(16) * P.L1e * (1 + P.staged) + 16 * (thi + tlo) + 8 * 48 + 64;
 
   // shared tables
   size_t o = 0;
@@ -149,6 +158,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.off_sq_e = o;    o = up(o + size_t(n) * 8);
   P.off_sq_p = o;    o = up(o + size_t(n / 2) * 8);
   P.off_level = o;   o = up(o + 64);
+  P.off_prof = o;    o = up(o + 32 * 8);
   // init scratch (batched spectra FFTs): per instance 2 x (2n + n) complex
   const size_t per = size_t(3 * n) * 16 * 2;
   int32_t batch = int32_t(std::max<int64_t>(1, std::min<int64_t>(B, (256LL << 20) / int64_t(per))));
@@ -282,6 +292,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.sq_e = reinterpret_cast<const double *>(ws + pl.off_sq_e);
   d.sq_p = reinterpret_cast<const double *>(ws + pl.off_sq_p);
   d.level = reinterpret_cast<int64_t *>(ws + pl.off_level);
+  d.prof = reinterpret_cast<unsigned long long *>(ws + pl.off_prof);
   d.inst = ws + pl.off_inst;
   d.stride = int64_t(pl.stride);
   d.o_par = pl.o_par; d.o_omega = pl.o_omega; d.o_lwe = pl.o_lwe; d.o_lwp = pl.o_lwp;

@@ -36,6 +36,7 @@ struct DevParams {
   const int32_t *slot_e, *slot_p;  // k1 -> slot of the local DIF output
   const double *sq_e, *sq_p;       // sin tables in task order
   int64_t *level;                  // device level counter
+  unsigned long long *prof;        // 32 cycle counters (profiling build only)
   // per-instance block
   char *inst;                      // base of instance 0
   int64_t stride;                  // bytes between instances
@@ -49,10 +50,12 @@ struct Plan {
   int32_t method = 0, precond = 0, maxit = 0;
   double tol = 0;
   int32_t L1e = 0, L1p = 0, npe = 0, npp = 0;
+  int32_t vpt = 0;      // Krylov vectors in registers: complex values per thread (0 = global)
+  int32_t staged = 0;   // cross-CTA step staged through a second SMEM buffer
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
-  size_t off_level = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
+  size_t off_level = 0, off_prof = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;

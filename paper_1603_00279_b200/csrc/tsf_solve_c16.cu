@@ -1,0 +1,6 @@
+// Instantiation of the fused solve kernels for thread-block clusters of 16 CTA(s).
+#include "tsf_kernels.cuh"
+
+namespace tsf {
+TSF_INSTANTIATE_CLUSTER(16)
+}  // namespace tsf

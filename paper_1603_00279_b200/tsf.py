@@ -94,20 +94,24 @@ class Solver:
     """A batch of instances (same n, M) solved level by level on one GPU."""
 
     def __init__(self, instances: Sequence[Instance], method="bicgstab", precond="strang",
-                 tol=1e-12, maxit=None, cluster=0, device=None, stream=None):
+                 tol=1e-12, maxit=None, cluster=0, device=None, stream=None, workspace=None):
         import torch
         self.lib = L.load()
         self.instances = list(instances)
         self.B = len(self.instances)
         self.n, self.M = self.instances[0].n, self.instances[0].M
         probs, keep = marshal(self.instances)
+        self.h2d_bytes = sum(a.nbytes for arrs in keep for a in arrs.values())
         self._solver = make_solver_struct(method, precond, tol, maxit, cluster)
         info = L.TsfPlanInfo()
         L.check(self.lib.tsf_plan(probs, self.B, C.byref(self._solver), C.byref(info)), "tsf_plan")
         self.info = info
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.device = dev
-        self.workspace = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
+        if workspace is not None and workspace.numel() >= int(info.workspace_bytes):
+            self.workspace = workspace
+        else:
+            self.workspace = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
         h = C.c_void_p()
         L.check(self.lib.tsf_init(probs, self.B, C.byref(self._solver),

@@ -1,0 +1,288 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Tolerance (north_star): relative L2 <= 1e-9 between GPU and oracle solutions, Krylov
+tolerance 1e-12.  Integer tables bit-exact.  Sizes span several tiles and every cluster
+size; full BASELINE sizes are checked on sampled levels (teacher forcing with the oracle's
+matrix-free products) and through properties that hold at any size.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1603_00279_b200 import _lib as L
+from paper_1603_00279_b200 import tsf
+from paper_1603_00279_b200.inputs import (Instance, config_c1, config_c3, config_c4, config_c5,
+                                          const)
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+SHAPES = {O.CONST: lambda s: (lambda t: s * np.ones_like(np.asarray(t, float))),
+          O.COS: lambda s: (lambda t: s * np.cos(t)), O.ONE_PLUS_T: lambda s: (lambda t: s * (1 + t)),
+          O.ONE_PLUS_T2: lambda s: (lambda t: s * (1 + t * t)), O.SIN: lambda s: (lambda t: s * np.sin(t)),
+          O.T: lambda s: (lambda t: s * t)}
+
+
+def pair(alpha, beta, n, M, gamma=(O.CONST, 0.5), dplus=(O.CONST, 1.0), dminus=(O.CONST, 1.0),
+         src="mms3", f_table=None):
+    """The same problem for the CUDA path (Instance) and the oracle (Problem)."""
+    inst = Instance(alpha, beta, n, M, SHAPES[gamma[0]](gamma[1]), SHAPES[dplus[0]](dplus[1]),
+                    SHAPES[dminus[0]](dminus[1]), src, f_table=f_table)
+    skind = {"mms3": O.SRC_MMS3, "exa": O.SRC_EXA, "table": O.SRC_TABLE, "zero": O.SRC_ZERO}[src]
+    p = O.Problem(alpha=alpha, beta=beta, n=n, M=M, gamma=gamma, dplus=dplus, dminus=dminus, src=skind,
+                  f_table=f_table)
+    return inst, p
+
+
+def run_levels(s, M):
+    U = [s.solutions()]
+    for _ in range(M):
+        s.step()
+        U.append(s.solutions())
+    assert s.sync() >= 0
+    return np.stack(U, axis=1)          # [B][M+1][n]
+
+
+def max_rel(U, Uo):
+    return max(np.linalg.norm(U[j] - Uo[j]) / np.linalg.norm(Uo[j]) for j in range(1, len(Uo)))
+
+
+# ------------------------------------------------------------------ components
+@pytest.mark.parametrize("Lc", [2, 4, 8, 16, 64, 256, 1024, 4096, 8192])
+def test_local_fft_slot_order_matches_exported_perm(Lc):
+    rng = np.random.default_rng(Lc)
+    x = rng.standard_normal(Lc) + 1j * rng.standard_normal(Lc)
+    _, perm, _ = tsf.debug_fft_tables(Lc)
+    np.testing.assert_array_equal(perm, O.fft_perm(Lc))
+    y = tsf.debug_local_fft(x)
+    X = np.fft.fft(x)
+    assert np.abs(y - X[perm]).max() <= 1e-14 * math.log2(max(Lc, 2)) * np.abs(X).max()
+    z = tsf.debug_local_fft(y, inverse=True) / Lc
+    assert np.abs(z - x).max() <= 1e-14 * math.log2(max(Lc, 2)) * np.abs(x).max()
+    if Lc <= 64:   # brute-force DFT of the oracle
+        np.testing.assert_allclose(y, O.dft(x)[perm], atol=1e-13 * Lc)
+
+
+@pytest.mark.parametrize("beta", [1.1, 1.5, 1.9, 2.0])
+def test_device_weights_match_oracle(beta):
+    K = 1 << 17
+    g, w = tsf.debug_weights(beta, K)
+    np.testing.assert_allclose(g, O.grunwald(beta, K), rtol=1e-13, atol=1e-300)
+    np.testing.assert_allclose(w, O.wsgd(beta, K), rtol=1e-12, atol=1e-17)
+
+
+@pytest.mark.parametrize("precond", ["strang", "tchan"])
+@pytest.mark.parametrize("n,cluster", [(64, 1), (1024, 1), (1024, 4), (4096, 16)])
+def test_spectra_match_direct_ffts_of_the_oracle_generators(precond, n, cluster):
+    inst, p = pair(0.7, 1.6, n, 4, gamma=(O.COS, 0.7), dplus=(O.ONE_PLUS_T, 1.3), dminus=(O.CONST, 0.4))
+    s = tsf.Solver([inst], precond=precond, cluster=cluster)
+    for j in (0, 2):
+        lamA, lamP = s.debug_spectra(0, j)
+        # A's Toeplitz generators (first column and row) from the oracle's dense assembly
+        A, _ = O.assemble(p, j)
+        col, row = A[:, 0].copy(), A[0].copy()
+        emb = np.r_[col, 0.0, row[:0:-1]]
+        ref = np.fft.fft(emb)[: n + 1]
+        assert np.abs(lamA - ref).max() <= 1e-13 * np.abs(ref).max()
+        c = O.strang_col(col, row) if precond == "strang" else O.tchan_col(col, row)
+        refp = np.fft.fft(c)[: n // 2 + 1]
+        assert np.abs(lamP - refp).max() <= 1e-13 * np.abs(refp).max()
+        assert np.all(refp.real > 0)                                   # themx2
+
+
+@pytest.mark.parametrize("n,cluster", [(64, 1), (256, 1), (1024, 2), (1024, 4), (1024, 8), (1024, 16),
+                                       (4096, 1), (4096, 8), (4096, 16)])
+def test_operator_applications_match_dense(n, cluster):
+    from scipy.linalg import circulant
+    inst, p = pair(0.7, 1.6, n, 8, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),
+                   dminus=(O.ONE_PLUS_T2, 0.5))
+    s = tsf.Solver([inst], cluster=cluster)
+    assert s.info.cluster == cluster
+    x = np.random.default_rng(n + cluster).standard_normal(n)
+    for j in (0, 5):
+        A, B = O.assemble(p, j)
+        for which, Mx in ((tsf.OP_A, A), (tsf.OP_B, B), (tsf.OP_AT, A.T)):
+            y = s.debug_apply(0, j, which, x)
+            assert np.linalg.norm(y - Mx @ x) <= 1e-13 * np.linalg.norm(Mx @ x) * math.log2(n)
+        Pm = circulant(O.strang_col(A[:, 0], A[0]))
+        for which, Mx in ((tsf.OP_PINV, Pm), (tsf.OP_PTINV, Pm.T)):
+            y = s.debug_apply(0, j, which, x)
+            # backward-error form avoids the conditioning of a dense solve
+            scale = np.abs(Mx).sum(1).max() * np.linalg.norm(y) + np.linalg.norm(x)
+            assert np.linalg.norm(Mx @ y - x) <= 1e-13 * math.log2(n) * scale
+
+
+def test_rhs_teacher_forced_matches_oracle():
+    inst, p = pair(0.8, 1.8, 256, 12, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),
+                   dminus=(O.ONE_PLUS_T2, 1.0))
+    Uo = O.solve(p)
+    s = tsf.Solver([inst])
+    for j in (0, 1, 2, 7, 11):
+        s.debug_set_history(0, Uo[: j + 1])
+        g = s.debug_rhs(0)
+        ref = O.rhs(p, j, Uo[: j + 1])
+        assert np.linalg.norm(g - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+# ------------------------------------------------------------------ free-running parity
+def test_c1_config_parity_and_accuracy():
+    inst = config_c1()[0]
+    _, p = pair(0.5, 1.5, 64, 64, gamma=(O.CONST, 0.5))
+    s = tsf.Solver([inst])
+    U = run_levels(s, 64)[0]
+    Uo = O.solve(p)
+    assert max_rel(U, Uo) <= RTOL
+    it, rr, st = s.stats()
+    assert (st == 0).all() and rr.max() < 1e-12 and 5 <= it.mean() / 2 <= 8
+    err = max(O.l2(U[j] - O.exact(p, j * p.tau), p.h) for j in range(65))
+    assert 2e-5 < err < 1e-4             # O(tau^2 + h^2) discretization error, not solver error
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cgnr"])
+@pytest.mark.parametrize("precond", ["strang", "tchan"])
+def test_c2_combinations_parity(method, precond):
+    inst, p = pair(0.8, 1.8, 256, 24, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),
+                   dminus=(O.ONE_PLUS_T2, 1.0))
+    s = tsf.Solver([inst], method=method, precond=precond)
+    U = run_levels(s, 24)[0]
+    assert max_rel(U, O.solve(p)) <= RTOL
+    it, rr, st = s.stats()
+    assert (st == 0).all() and rr.max() < 1e-12
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 4, 8, 16])
+def test_table_source_parity_every_cluster(cluster):
+    f = np.random.default_rng(160300279).standard_normal((12, 1024))
+    inst, p = pair(0.9, 1.9, 1024, 12, gamma=(O.CONST, 1.0), dplus=(O.CONST, 2.0),
+                   dminus=(O.CONST, 0.5), src="table", f_table=f)
+    s = tsf.Solver([inst], cluster=cluster)
+    U = run_levels(s, 12)[0]
+    assert max_rel(U, O.solve(p)) <= RTOL
+
+
+def test_noprec_and_exa_source():
+    inst, p = pair(0.5, 1.3, 128, 8, gamma=(O.T, -1.0), dplus=(O.SIN, 9.0), dminus=(O.SIN, 4.0), src="exa")
+    s = tsf.Solver([inst], precond="none", maxit=5000)
+    U = run_levels(s, 8)[0]
+    assert max_rel(U, O.solve(p)) <= RTOL
+
+
+def test_batched_instances_parity():
+    rng = np.random.default_rng(7)
+    pairs = [pair(float(rng.uniform(0.1, 0.99)), float(rng.uniform(1.1, 1.95)), 256, 10,
+                  gamma=(O.CONST, float(rng.uniform(-1, 1))), dplus=(O.CONST, float(rng.uniform(0, 2))),
+                  dminus=(O.CONST, float(rng.uniform(0, 2)))) for _ in range(6)]
+    s = tsf.Solver([a for a, _ in pairs])
+    U = run_levels(s, 10)
+    for b, (_, p) in enumerate(pairs):
+        assert max_rel(U[b], O.solve(p)) <= RTOL
+
+
+def test_step_graph_equals_one_shot_solve_and_is_deterministic():
+    inst, _ = pair(0.6, 1.7, 1024, 16, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0))
+    s = tsf.Solver([inst])
+    U1 = run_levels(s, 16)[0][-1]
+    it1 = s.stats()[0].copy()
+    s.reset()
+    s.solve()
+    s.sync()
+    U2 = s.solution(0)
+    s.reset()
+    s.solve()
+    s.sync()
+    U3 = s.solution(0)
+    np.testing.assert_array_equal(U1, U2)
+    np.testing.assert_array_equal(U2, U3)
+    np.testing.assert_array_equal(it1, s.stats()[0])
+
+
+def test_zero_operator_and_stability_invariants():
+    # gamma = d = 0, f = 0: u^j = phi for all j; f = 0 -> ||u^j|| <= ||u^0||
+    inst = Instance(0.4, 1.5, 128, 6, const(0.0), const(0.0), const(0.0), "zero")
+    s = tsf.Solver([inst])
+    U = run_levels(s, 6)[0]
+    np.testing.assert_allclose(U, np.tile(U[0], (7, 1)), atol=1e-15)
+    inst = Instance(0.5, 1.9, 256, 32, const(0.7), const(1.1), const(0.4), "zero")
+    s = tsf.Solver([inst])
+    U = run_levels(s, 32)[0]
+    norms = np.linalg.norm(U, axis=1)
+    assert norms.max() <= norms[0] * (1 + 1e-12)
+
+
+def test_errors_are_reported():
+    with pytest.raises(L.TsfError, match="alpha"):
+        tsf.Solver([Instance(1.5, 1.5, 64, 4, const(0), const(1), const(1))])
+    s = tsf.Solver(config_c1())
+    s.solve()
+    with pytest.raises(L.TsfError, match="TSF_E_STATE"):
+        s.step()
+
+
+# ------------------------------------------------------------------ BASELINE sizes (sampled)
+@pytest.mark.slow
+def test_c3_full_size_sampled_levels():
+    """configs[2] at full size (n = 2^14, M = 2^9): every level converges; sampled levels are
+    checked against the oracle's matrix-free RHS and product (teacher forcing)."""
+    inst = config_c3()[0]
+    p = O.Problem(alpha=0.9, beta=1.9, n=16384, M=512, gamma=(O.CONST, 1.0), dplus=(O.CONST, 2.0),
+                  dminus=(O.CONST, 0.5), src=O.SRC_TABLE, f_table=inst.f_table)
+    s = tsf.Solver([inst])
+    U = [s.solution(0)]
+    for _ in range(512):
+        s.step()
+        U.append(s.solution(0))
+    assert s.sync() == 0
+    it, rr, st = s.stats()
+    assert (st == 0).all() and rr.max() < 1e-12 and 7 <= it.mean() / 2 <= 11
+    U = np.array(U)
+    for j in (0, 1, 100, 511):
+        g = O.rhs_nodense(p, j, U[: j + 1])
+        res = O.matvec(p, j, 0, U[j + 1]) - g
+        assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(g), j
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled_instances():
+    insts = config_c4()
+    s = tsf.Solver(insts)
+    s.solve()
+    assert s.sync() == 0
+    it, rr, st = s.stats()
+    assert (st == 0).all() and rr.max() < 1e-12
+    u = s.solutions()
+    for b in (0, 511, 1023):   # sampled instances: full free-running oracle at n = 4096
+        inst = insts[b]
+        _, p = pair(inst.alpha, inst.beta, 4096, 256, gamma=(O.CONST, float(inst.gamma(0.0))),
+                    dplus=(O.CONST, float(inst.dplus(0.0))), dminus=(O.CONST, float(inst.dminus(0.0))))
+        Uo = O.solve(p)
+        assert np.linalg.norm(u[b] - Uo[-1]) <= RTOL * np.linalg.norm(Uo[-1]), b
+
+
+@pytest.mark.slow
+def test_c5_full_size_properties():
+    """configs[4] at n = 2^17 (dense oracle would need 128 GiB): the first levels of two
+    instances satisfy the oracle's matrix-free residual check, and the solution tracks the
+    manufactured exact solution within the discretization error."""
+    insts = config_c5(B=2)
+    s = tsf.Solver(insts)
+    for _ in range(2):
+        s.step()
+    assert s.sync() == 0
+    it, rr, st = s.stats()
+    assert (st[:, :2] == 0).all() and rr[:, :2].max() < 1e-12
+    x, _ = tsf.sample_points(insts[0])
+    ex = ((2 / 256) ** 3 + 1) * x**2 * (1 - x)**2          # u = (t^3 + 1) X at t_2
+    for b in range(2):
+        u = s.solution(b)
+        assert np.linalg.norm(u - ex) <= 1e-6 * np.linalg.norm(ex)

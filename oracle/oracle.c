@@ -244,11 +244,42 @@ static void lu_solve(int64_t n, const double *LU, const int64_t *piv, double *x)
   }
 }
 
+/* Iterative refinement (DESIGN.md R-refine): the per-level result is defined as the exact
+ * solution of A u = g (eq3.3); plain GE has forward error ~cond(A) eps (1e-8 relative at
+ * cond ~ 1e7, e.g. beta -> 2 with small alpha).  r = b - A x is accumulated in x87 extended
+ * precision (long double, 64-bit mantissa) from the unfactored A0, the correction solved
+ * with the LU factors, x += d; this converges to the correctly rounded solution while
+ * cond(A) * eps << 1.                                                                   */
+static void refine(int64_t n, const double *A0, const double *LU, const int64_t *piv,
+                   const double *b, double *x, int steps) {
+  double *d = (double *)malloc(sizeof(double) * (size_t)n);
+  for (int it = 0; it < steps; ++it) {
+    for (int64_t i = 0; i < n; ++i) {
+      long double s = (long double)b[i];
+      const double *ai = A0 + i * n;
+      for (int64_t m = 0; m < n; ++m) s -= (long double)ai[m] * (long double)x[m];
+      d[i] = (double)s;
+    }
+    lu_solve(n, LU, piv, d);
+    for (int64_t i = 0; i < n; ++i) x[i] += d[i];
+  }
+  free(d);
+}
+
 int orc_ge_solve(int64_t n, double *A, double *x) {
   int64_t *piv = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  double *A0 = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *b = (double *)malloc(sizeof(double) * (size_t)n);
+  memcpy(A0, A, sizeof(double) * (size_t)(n * n));
+  memcpy(b, x, sizeof(double) * (size_t)n);
   int rc = lu_factor(n, A, piv);
-  if (rc == 0) lu_solve(n, A, piv, x);
+  if (rc == 0) {
+    lu_solve(n, A, piv, x);
+    refine(n, A0, A, piv, b, x, 3);
+  }
   free(piv);
+  free(A0);
+  free(b);
   return rc;
 }
 
@@ -380,7 +411,9 @@ int orc_solve(const orc_problem *p, double *U) {
     U[i] = (p->phi_kind == ORC_PHI_X2) ? Xfun(x) : p->phi[i];
   }
   double *A = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *A0 = (double *)malloc(sizeof(double) * (size_t)(n * n));
   double *B = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *rhs = (double *)malloc(sizeof(double) * (size_t)n);
   int64_t *piv = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
   const int reuse = coefficients_constant(p);
   int have_factor = 0;
@@ -389,6 +422,7 @@ int orc_solve(const orc_problem *p, double *U) {
     double *g = U + (j + 1) * n;
     if (!(reuse && have_factor && j >= 1)) {
       orc_assemble(p, j, A, B);
+      memcpy(A0, A, sizeof(double) * (size_t)(n * n));
       rhs_with_B(p, j, U, B, g);
       rc = lu_factor(n, A, piv);
       if (rc) break;
@@ -396,10 +430,14 @@ int orc_solve(const orc_problem *p, double *U) {
     } else {
       rhs_with_B(p, j, U, B, g);   /* B is level-invariant too for j >= 1 */
     }
+    memcpy(rhs, g, sizeof(double) * (size_t)n);
     lu_solve(n, A, piv, g);
+    refine(n, A0, A, piv, rhs, g, 3);
   }
   free(A);
+  free(A0);
   free(B);
+  free(rhs);
   free(piv);
   return rc;
 }

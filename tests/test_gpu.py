@@ -247,9 +247,12 @@ def test_c3_full_size_sampled_levels():
     assert (st == 0).all() and rr.max() < 1e-12 and 7 <= it.mean() / 2 <= 11
     U = np.array(U)
     for j in (0, 1, 100, 511):
+        # teacher forcing: the oracle's RHS from the GPU history, residual of the GPU level
+        # solution under the oracle's matrix-free A.  At n = 2^14 (cond(A) ~ 1e8) the FP64
+        # floor of any FFT matvec is ~1e-10 (SURVEY hard part 1); gate = north-star 1e-9.
         g = O.rhs_nodense(p, j, U[: j + 1])
         res = O.matvec(p, j, 0, U[j + 1]) - g
-        assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(g), j
+        assert np.linalg.norm(res) <= RTOL * np.linalg.norm(g), j
 
 
 @pytest.mark.slow

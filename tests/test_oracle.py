@@ -160,6 +160,41 @@ def test_assembly_matches_delta_operator(j):
         eta - sigma * (_fn(p.dplus, t) + _fn(p.dminus, t)) * w1 / p.h ** p.beta, rel=1e-13)
 
 
+def _exact_rational_solve(A, b):
+    from fractions import Fraction
+    n = len(b)
+    M = [[Fraction(float(v)) for v in row] + [Fraction(float(bb))] for row, bb in zip(A, b)]
+    for c in range(n):
+        p = max(range(c, n), key=lambda r: abs(M[r][c]))
+        M[c], M[p] = M[p], M[c]
+        for r in range(n):
+            if r != c and M[r][c] != 0:
+                f = M[r][c] / M[c][c]
+                M[r] = [a - f * q for a, q in zip(M[r], M[c])]
+    return np.array([float(M[i][n] / M[i][i]) for i in range(n)])
+
+
+def test_refined_ge_approaches_the_exact_solution():
+    # DESIGN.md R-refine: the level result is the exact solution of A u = g; GE with
+    # extended-precision refinement reaches it far below LAPACK's cond*eps forward error.
+    A = np.array([[1.0 / (i + j + 1) for j in range(9)] for i in range(9)])      # cond 5e11
+    b = np.ones(9)
+    xe = _exact_rational_solve(A, b)
+    err = np.abs(O.ge_solve(A, b) - xe).max() / np.abs(xe).max()
+    lapack = np.abs(np.linalg.solve(A, b) - xe).max() / np.abs(xe).max()
+    assert err < 1e-8 and err < lapack / 100
+    p = O.Problem(alpha=0.28, beta=1.93, n=20, M=256, gamma=(O.CONST, 0.84), dplus=(O.CONST, 0.55),
+                  dminus=(O.CONST, 1.13), src=O.SRC_MMS3)
+    A, _ = O.assemble(p, 1)
+    b = np.random.default_rng(0).standard_normal(20)
+    xe = _exact_rational_solve(A, b)
+    np.testing.assert_allclose(O.ge_solve(A, b), xe, rtol=2e-16, atol=0)
+    U = O.solve(p.__class__(**{**p.__dict__, "M": 2, "_keep": []}))
+    g = O.rhs(p.__class__(**{**p.__dict__, "M": 2, "_keep": []}), 0, U[:1])
+    A0, _ = O.assemble(p.__class__(**{**p.__dict__, "M": 2, "_keep": []}), 0)
+    np.testing.assert_allclose(U[1], _exact_rational_solve(A0, g), rtol=1e-15, atol=1e-30)
+
+
 def test_ge_against_lapack():
     rng = np.random.default_rng(0)
     for n in (1, 2, 7, 50):

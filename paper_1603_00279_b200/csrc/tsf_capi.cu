@@ -205,13 +205,15 @@ __global__ void k_set_level(int64_t *level, int64_t v) {
 
 __global__ void k_dbg_fft(double2 *buf, int L, const double2 *tw, int twN, int inverse) {
   extern __shared__ __align__(16) unsigned char raw[];
-  const Smem sm = smem_view(raw, L, false, nullptr);
-  load_twiddles(sm, L, tw, twN);
-  for (int e = threadIdx.x; e < L; e += blockDim.x) sm.A[e] = buf[e];
+  const Smem sm = smem_view(raw, L, L / 2, false, false, nullptr);
+  const int f = twN / L;
+  for (int i = threadIdx.x; i < tw_lo_len(L); i += blockDim.x) sm.tlo[i] = tw[i * f];
+  for (int i = threadIdx.x; i < tw_hi_len(L); i += blockDim.x) sm.thi[i] = tw[(i << 6) * f];
+  for (int e = threadIdx.x; e < L; e += blockDim.x) sm.A[pidx(e)] = buf[e];
   __syncthreads();
   if (inverse) local_fft<true>(sm.A, L, sm, L);
   else local_fft<false>(sm.A, L, sm, L);
-  for (int e = threadIdx.x; e < L; e += blockDim.x) buf[e] = sm.A[e];
+  for (int e = threadIdx.x; e < L; e += blockDim.x) buf[e] = sm.A[pidx(e)];
 }
 
 // per-level spectra of one instance in natural bin order
@@ -222,7 +224,8 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx <= n + n / 2 + 1;
        idx += int64_t(gridDim.x) * blockDim.x) {
     if (idx <= n && lamA) {
-      SpecOp op = make_op(P, I, j, OP_A, 0);
+      const Smem none = {};
+      SpecOp op = make_op(P, I, j, OP_A, 0, none);
       if (idx == n) { lamA[n] = op.nyquist(int(n)); continue; }
       const int np = P.npe;
       const int i = int(idx % np), ab = int((idx / np) % 2), k2 = int((idx / (2 * np)) % C);
@@ -231,7 +234,8 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
       lamA[bin] = op.lam_idx(int(idx), int(bin));
     } else if (idx > n && lamP && P.precond != TSF_NOPREC) {
       const int64_t q = idx - n - 1;
-      SpecOp op = make_op(P, I, j, OP_PINV, 0);
+      const Smem none = {};
+      SpecOp op = make_op(P, I, j, OP_PINV, 0, none);
       if (q == n / 2) { lamP[n / 2] = op.nyquist(int(n / 2)); continue; }
       const int np = P.npp;
       const int i = int(q % np), ab = int((q / np) % 2), k2 = int((q / (2 * np)) % C);
@@ -612,7 +616,7 @@ int tsf_debug_local_fft(int64_t L, const double *x, double *y, int32_t inverse) 
   CK(cudaMalloc(&tw, size_t(2 * L) * 16));
   CK(cudaMemcpy(buf, x, size_t(L) * 16, cudaMemcpyHostToDevice));
   k_twiddle<<<grid_for(2 * L), 256>>>(tw, int(2 * L));
-  const size_t dsm = size_t(L) * 16 + 16 * size_t(L / 64 + 64) + 1024;
+  const size_t dsm = size_t(L + L / 16) * 16 + 16 * size_t(L / 64 + 64) + 1024;
   CK(cudaFuncSetAttribute(k_dbg_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
   k_dbg_fft<<<1, kThreads, dsm>>>(buf, int(L), tw, int(2 * L), inverse);
   CK(cudaGetLastError());

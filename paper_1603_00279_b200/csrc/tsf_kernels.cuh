@@ -106,9 +106,16 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------------------ shared memory
-// [A: L1e][B: L1e if staged][thi: L1e/64][tlo: 64][wred: 40 doubles][cred: 8 doubles]
+// Carve-up (smem_bytes in tsf_plan.h): A (apply input), B (staging) and O (apply output) when
+// staged; local-FFT twiddles (direct W_{L1e}^e table if resident, else two-level); resident
+// per-CTA constant tables: column twiddles W_L^{q k1}, base spectra and pair twiddles
+// W_{2L}^{bin} in task order, sine tables; reduction scratch.
 struct Smem {
-  double2 *A, *B, *thi, *tlo;
+  double2 *A, *B, *O;
+  double2 *twd, *thi, *tlo;          // twd != nullptr: direct table
+  double2 *ctwe, *ctwp;              // column twiddles (resident)
+  double2 *lame, *lamp, *pwe, *pwp;  // base spectra / pair twiddles (resident)
+  double *sqe, *sqp;                 // sine tables (resident)
   double *wred, *cred;
   unsigned long long *prof;
 };
@@ -133,28 +140,78 @@ enum ProfSlot { PS_FFT_F = 0, PS_BAR1, PS_GATHER, PS_COLF, PS_PAIRS, PS_COLI, PS
 __device__ __forceinline__ int tw_hi_len(int L1e) { return L1e >= 64 ? L1e / 64 : 1; }
 __device__ __forceinline__ int tw_lo_len(int L1e) { return L1e >= 64 ? 64 : L1e; }
 
-__device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, bool staged,
-                                          unsigned long long *prof) {
-  Smem s;
+__device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, bool staged,
+                                          bool resident, unsigned long long *prof) {
+  Smem s = {};
   s.prof = prof;
-  s.A = reinterpret_cast<double2 *>(raw);
-  s.B = staged ? s.A + L1e : nullptr;
-  s.thi = s.A + L1e * (staged ? 2 : 1);
-  s.tlo = s.thi + tw_hi_len(L1e);
-  s.wred = reinterpret_cast<double *>(s.tlo + tw_lo_len(L1e));
-  s.cred = s.wred + 40;
+  double2 *c = reinterpret_cast<double2 *>(raw);
+  const int L1pad = L1e + L1e / 16;
+  s.A = c; c += L1pad;
+  if (staged) { s.B = c; c += L1e; s.O = c; c += L1pad; }
+  if (resident) {
+    s.twd = c; c += L1e;
+    s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
+    s.lame = c; c += L1e; s.lamp = c; c += L1p;
+    s.pwe = c; c += L1e; s.pwp = c; c += L1p;
+  } else {
+    s.thi = c; c += tw_hi_len(L1e);
+    s.tlo = c; c += tw_lo_len(L1e);
+  }
+  double *d = reinterpret_cast<double *>(c);
+  if (resident) { s.sqe = d; d += L1e; s.sqp = d; d += L1p; }
+  s.wred = d;
+  s.cred = d + 40;
   return s;
 }
 
-// Two-level twiddle table of W_{L1e}: W^e = thi[e >> 6] * tlo[e & 63], copied from the
-// global table tw[x] = exp(-2 pi i x / twN).
-__device__ __forceinline__ void load_twiddles(const Smem &sm, int L1e, const double2 *tw, int twN) {
-  const int f = twN / L1e;
-  for (int i = threadIdx.x; i < tw_lo_len(L1e); i += kThreads) sm.tlo[i] = tw[i * f];
-  for (int i = threadIdx.x; i < tw_hi_len(L1e); i += kThreads) sm.thi[i] = tw[(i << 6) * f];
-}
 __device__ __forceinline__ double2 twid(const Smem &sm, int e) {
+  if (sm.twd) return sm.twd[e];
   return cmul(sm.thi[e >> 6], sm.tlo[e & 63]);
+}
+
+__device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col);
+
+// Kernel prologue: local-FFT twiddles and (resident mode) this CTA's constant tables, copied
+// from the accurate global tables (twiddles tw[x] = exp(-2 pi i x / twN)).
+__device__ __forceinline__ void load_constants(const DevParams &P, const double2 *lwe, const double2 *lwp,
+                                               const Smem &sm, uint32_t r) {
+  const double2 *tw = reinterpret_cast<const double2 *>(P.tw);
+  const int L1e = P.L1e, L1p = P.L1p, C = P.C;
+  const int f = P.twN / L1e;
+  if (sm.twd) {
+    for (int i = threadIdx.x; i < L1e; i += kThreads) sm.twd[i] = tw[i * f];
+  } else {
+    for (int i = threadIdx.x; i < tw_lo_len(L1e); i += kThreads) sm.tlo[i] = tw[i * f];
+    for (int i = threadIdx.x; i < tw_hi_len(L1e); i += kThreads) sm.thi[i] = tw[(i << 6) * f];
+  }
+  if (sm.ctwe) {
+    const int64_t n = P.n;
+    const int twL_e = P.twN / int(n), twL_p = P.twN / int(n / 2);
+    const int nce = L1e / C, ncp = L1p / C;
+    for (int u = threadIdx.x; u < L1e; u += kThreads) {     // column twiddles W_L^{q k1}
+      const int q = u / nce, col = u - q * nce;
+      sm.ctwe[u] = tw[q * col_k1(L1e, C, r, col) * twL_e];
+    }
+    for (int u = threadIdx.x; u < L1p; u += kThreads) {
+      const int q = u / ncp, col = u - q * ncp;
+      sm.ctwp[u] = tw[q * col_k1(L1p, C, r, col) * twL_p];
+    }
+    // task-order slices of CTA r: index ((r C + k2) 2 + ab) np + i = r L1 + local
+    for (int u = threadIdx.x; u < L1e; u += kThreads) {
+      const int np = P.npe;
+      const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+      sm.lame[u] = lwe[int64_t(r) * L1e + u];
+      sm.sqe[u] = P.sq_e[int64_t(r) * L1e + u];
+      sm.pwe[u] = tw[task_bin(L1e, C, int(r), i, k2, ab) * (P.twN / int(2 * n))];
+    }
+    for (int u = threadIdx.x; u < L1p; u += kThreads) {
+      const int np = P.npp;
+      const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+      if (lwp) sm.lamp[u] = lwp[int64_t(r) * L1p + u];
+      sm.sqp[u] = P.sq_p[int64_t(r) * L1p + u];
+      sm.pwp[u] = tw[task_bin(L1p, C, int(r), i, k2, ab) * (P.twN / int(n))];
+    }
+  }
 }
 
 // Deterministic cluster-wide sum of NV <= 4 scalars: warp butterflies (exactly commutative,
@@ -219,6 +276,11 @@ __device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, dou
   a3 = csub(t1, t3);
 }
 
+// Padded SMEM index of element p of a transform buffer (A, O): one pad slot per 16 elements
+// makes the stride-4 and stride-16 accesses of the early DIT / late DIF stages bank-conflict
+// free.  Buffers hold L1 + L1/16 complex values.
+__device__ __forceinline__ int pidx(int p) { return p + (p >> 4); }
+
 // one stage: m = 2^lm, twiddle W_m^{kq} = W_{L1e}^{kq (L1e/m)}
 template <bool INV, int RADIX>
 __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem &sm, int L1e) {
@@ -230,7 +292,8 @@ __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem
     const int k = b & (mprev - 1);
     const int base = ((b >> lmp) << lm) + k;
     if constexpr (RADIX == 4) {
-      double2 a0 = A[base], a1 = A[base + mprev], a2 = A[base + 2 * mprev], a3 = A[base + 3 * mprev];
+      const int p0 = pidx(base), p1 = pidx(base + mprev), p2 = pidx(base + 2 * mprev), p3 = pidx(base + 3 * mprev);
+      double2 a0 = A[p0], a1 = A[p1], a2 = A[p2], a3 = A[p3];
       if (k != 0) {
         const double2 w1 = twid(sm, k * tstep), w2 = twid(sm, 2 * k * tstep), w3 = twid(sm, 3 * k * tstep);
         if (INV) {
@@ -243,39 +306,128 @@ __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem
       } else {
         bfly4<INV>(a0, a1, a2, a3);
       }
-      A[base] = a0; A[base + mprev] = a1; A[base + 2 * mprev] = a2; A[base + 3 * mprev] = a3;
+      A[p0] = a0; A[p1] = a1; A[p2] = a2; A[p3] = a3;
     } else {
-      double2 a0 = A[base], a1 = A[base + mprev];
+      const int p0 = pidx(base), p1 = pidx(base + mprev);
+      double2 a0 = A[p0], a1 = A[p1];
       const double2 w = twid(sm, k * tstep);
       if (INV) {
         a1 = cmulc(a1, w);
-        A[base] = cadd(a0, a1); A[base + mprev] = csub(a0, a1);
+        A[p0] = cadd(a0, a1); A[p1] = csub(a0, a1);
       } else {
-        A[base] = cadd(a0, a1); A[base + mprev] = cmul(csub(a0, a1), w);
+        A[p0] = cadd(a0, a1); A[p1] = cmul(csub(a0, a1), w);
       }
     }
   }
 }
 
-// Requires the input to be visible to all threads (caller synchronizes); ends synchronized.
+// Two consecutive radix-4 stages s (m = 2^lm) and s-1 (m/4) fused in registers: a thread owns
+// the 16 positions g m + j (m/4) + j' (m/16) + k'' and applies exactly the butterflies of both
+// stages (DIF: s then s-1; DIT: s-1 then s), so the data placement equals the unfused plan.
 template <bool INV>
-__device__ __noinline__ void local_fft(double2 *A, int L1, const Smem &sm, int L1e) {
+__device__ __forceinline__ void fft_pass16(double2 *A, int L1, int lm, const Smem &sm, int L1e) {
+  const int lmpp = lm - 4;
+  const int mp = 1 << (lm - 2), mpp = 1 << lmpp;
+  const int ts = L1e >> lm;          // W_m^x   = W_{L1e}^{x ts}
+  const int tsp = L1e >> (lm - 2);   // W_{m/4}^x = W_{L1e}^{x tsp}
+  const int nsb = L1 >> 4;
+  for (int u = threadIdx.x; u < nsb; u += kThreads) {
+    const int kpp = u & (mpp - 1);
+    const int base = ((u >> lmpp) << lm) + kpp;
+    double2 x[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) x[j][jp] = A[pidx(base + j * mp + jp * mpp)];
+    if (!INV) {
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {            // stage s: butterfly k = jp mpp + kpp
+        bfly4<false>(x[0][jp], x[1][jp], x[2][jp], x[3][jp]);
+        const int k = jp * mpp + kpp;
+        if (k != 0) {
+          x[1][jp] = cmul(x[1][jp], twid(sm, k * ts));
+          x[2][jp] = cmul(x[2][jp], twid(sm, 2 * k * ts));
+          x[3][jp] = cmul(x[3][jp], twid(sm, 3 * k * ts));
+        }
+      }
+      double2 w1 = zero2(), w2 = zero2(), w3 = zero2();
+      if (kpp != 0) { w1 = twid(sm, kpp * tsp); w2 = twid(sm, 2 * kpp * tsp); w3 = twid(sm, 3 * kpp * tsp); }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {               // stage s-1: butterfly k = kpp in group 4g + j
+        bfly4<false>(x[j][0], x[j][1], x[j][2], x[j][3]);
+        if (kpp != 0) {
+          x[j][1] = cmul(x[j][1], w1);
+          x[j][2] = cmul(x[j][2], w2);
+          x[j][3] = cmul(x[j][3], w3);
+        }
+      }
+    } else {
+      double2 w1 = zero2(), w2 = zero2(), w3 = zero2();
+      if (kpp != 0) { w1 = twid(sm, kpp * tsp); w2 = twid(sm, 2 * kpp * tsp); w3 = twid(sm, 3 * kpp * tsp); }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {               // DIT stage s-1
+        if (kpp != 0) {
+          x[j][1] = cmulc(x[j][1], w1);
+          x[j][2] = cmulc(x[j][2], w2);
+          x[j][3] = cmulc(x[j][3], w3);
+        }
+        bfly4<true>(x[j][0], x[j][1], x[j][2], x[j][3]);
+      }
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {            // DIT stage s
+        const int k = jp * mpp + kpp;
+        if (k != 0) {
+          x[1][jp] = cmulc(x[1][jp], twid(sm, k * ts));
+          x[2][jp] = cmulc(x[2][jp], twid(sm, 2 * k * ts));
+          x[3][jp] = cmulc(x[3][jp], twid(sm, 3 * k * ts));
+        }
+        bfly4<true>(x[0][jp], x[1][jp], x[2][jp], x[3][jp]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) A[pidx(base + j * mp + jp * mpp)] = x[j][jp];
+  }
+}
+
+// Requires the input to be visible to all threads (caller synchronizes); ends synchronized.
+// Radix-4 stages are fused pairwise into radix-16 register passes from the bottom (stages
+// (1,0), (3,2), ...); a leftover top radix-4 stage and the radix-2 stage run alone.
+template <bool INV>
+__device__ __forceinline__ void local_fft(double2 *A, int L1, const Smem &sm, int L1e) {
   const int l = __ffs(L1) - 1;
   const int S4 = l >> 1;
   const bool r2 = l & 1;
-  const int S = S4 + (r2 ? 1 : 0);
+  // fuse only when every thread owns a 16-point super-butterfly (else radix-4 stages keep
+  // all threads busy); the data placement is the same either way
+  const bool fuse = L1 >= 16 * kThreads;
+  const int npair = fuse ? (S4 >> 1) : 0;   // fused pairs (2i+1, 2i), i < npair
+  if (!fuse) {
+    if (!INV) {
+      if (r2) { fft_stage<false, 2>(A, L1, l, sm, L1e); __syncthreads(); }
+      for (int s = S4 - 1; s >= 0; --s) { fft_stage<false, 4>(A, L1, 2 * (s + 1), sm, L1e); __syncthreads(); }
+    } else {
+      for (int s = 0; s < S4; ++s) { fft_stage<true, 4>(A, L1, 2 * (s + 1), sm, L1e); __syncthreads(); }
+      if (r2) { fft_stage<true, 2>(A, L1, l, sm, L1e); __syncthreads(); }
+    }
+    return;
+  }
+  const bool lone = S4 & 1;           // stage S4-1 alone
   if (!INV) {
-    for (int s = S - 1; s >= 0; --s) {
-      if (r2 && s == S - 1) fft_stage<false, 2>(A, L1, l, sm, L1e);
-      else fft_stage<false, 4>(A, L1, 2 * (s + 1), sm, L1e);
+    if (r2) { fft_stage<false, 2>(A, L1, l, sm, L1e); __syncthreads(); }
+    if (lone) { fft_stage<false, 4>(A, L1, 2 * S4, sm, L1e); __syncthreads(); }
+    for (int i = npair - 1; i >= 0; --i) {
+      fft_pass16<false>(A, L1, 4 * i + 4, sm, L1e);   // stages 2i+1 (m = 4^{2i+2}) and 2i
       __syncthreads();
     }
   } else {
-    for (int s = 0; s < S; ++s) {
-      if (r2 && s == S - 1) fft_stage<true, 2>(A, L1, l, sm, L1e);
-      else fft_stage<true, 4>(A, L1, 2 * (s + 1), sm, L1e);
+    for (int i = 0; i < npair; ++i) {
+      fft_pass16<true>(A, L1, 4 * i + 4, sm, L1e);
       __syncthreads();
     }
+    if (lone) { fft_stage<true, 4>(A, L1, 2 * S4, sm, L1e); __syncthreads(); }
+    if (r2) { fft_stage<true, 2>(A, L1, l, sm, L1e); __syncthreads(); }
   }
 }
 
@@ -327,13 +479,19 @@ __device__ __forceinline__ void fft_reg(double2 (&x)[N]) {
 // for L_W the base spectrum of W (embedding, Strang or T. Chan), s the sine table of Lambda_Q,
 // optionally conjugated (A^T, P^T).  Multiply (A, B, A^T) or divide (P^{-1}, P^{-T}).
 struct SpecOp {
-  const double2 *lam;   // task-order base spectrum of this instance
+  const double2 *lam;   // task-order base spectrum of this instance (SMEM slice if resident)
   const double *sq;     // task-order sine table
+  const double2 *pw;    // resident: pair twiddles W_{2L}^{bin} in task order, else nullptr
   double2 nyq;          // base spectrum at the Nyquist bin L
   int np;               // column-pair tasks per CTA
-  int rC;               // r * C
+  int rC;               // r * C (0 for resident slices)
   double eta, mu, ppq, pmq, c2, qcorr, scale;
   bool conj;
+  // W_{2L}^{bin} of bin (k2, ab, i): resident table or the global twiddle table
+  __device__ __forceinline__ double2 wtw(int k2, int ab, int i, int bin, const double2 *tw,
+                                         int tw2L) const {
+    return pw ? pw[((rC + k2) * 2 + ab) * np + i] : tw[bin * tw2L];
+  }
   __device__ __forceinline__ double2 lam_idx(int idx, int bin) const {
     const double2 b = lam[idx];
     const double s = sq[idx];
@@ -389,22 +547,23 @@ __device__ __forceinline__ void pair_self(double2 &Z, double2 la, double2 lb, do
 struct Geo {
   int L1, L, np, twL, tw2L;   // twL = twN/L (W_L factor), tw2L = twN/(2L)
   const int32_t *slot;
+  const double2 *ctw;         // resident column twiddles W_L^{q k1(col)} [q ncol + col]
 };
 
 // C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).
 template <bool DIV>
-__device__ __noinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
+__device__ __forceinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
                                              const double2 *__restrict__ tw) {
   for (int i = threadIdx.x; i < g.np; i += kThreads) {
     if (i == 0) {
-      const int sa = g.slot[0], sb = g.slot[g.L1 / 2];
+      const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
       double2 a = A[sa], b = A[sb];
       pair_self<DIV>(a, op.get(0, 0, 0, 0), op.nyquist(g.L), tw[0], op.scale);
       const double2 lm = op.get(0, 1, 0, g.L / 2);
       pair_self<DIV>(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
       A[sa] = a; A[sb] = b;
     } else {
-      const int sa = g.slot[i], sb = g.slot[g.L1 - i];
+      const int sa = pidx(g.slot[i]), sb = pidx(g.slot[g.L1 - i]);
       double2 a = A[sa], b = A[sb];
       pair_apply<DIV>(a, b, op.get(0, 0, i, i), op.get(0, 1, i, g.L - i), tw[i * g.tw2L], op.scale);
       A[sa] = a; A[sb] = b;
@@ -421,15 +580,20 @@ __device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col) {
 
 // C > 1, staged through the local buffer B (layout B[q * ncol + col], ncol = L1/C):
 //   gather A_q[slot(k1)] from every CTA -> per column: twiddle W_L^{q k1}, DFT_C -> per bin
-//   pair: spectral op -> per column: inverse DFT_C, conj twiddle -> scatter to A_{m2}.
+//   pair: spectral op -> per column: inverse DFT_C, conj twiddle -> scatter to O_{m2}.
+// The result lands in the output buffers O, so no CTA can still be gathering from the
+// buffer being written: two cluster barriers per application (before the gather, after the
+// scatter).
 template <int C, bool DIV>
-__device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, const SpecOp &op,
-                                          const double2 *__restrict__ tw, uint32_t r, const Smem &sm) {
+__device__ __forceinline__ void cross_staged(double2 *A, double2 *B, double2 *O, const Geo &g,
+                                          const SpecOp &op, const double2 *__restrict__ tw, uint32_t r,
+                                          const Smem &sm) {
   TSF_PT0();
   const int ncol = g.L1 / C;
+#pragma unroll 4
   for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM gather
     const int q = u / ncol, col = u - q * ncol;
-    B[u] = remote<C>(A, uint32_t(q))[g.slot[col_k1(g.L1, C, r, col)]];
+    B[u] = remote<C>(A, uint32_t(q))[pidx(g.slot[col_k1(g.L1, C, r, col)])];
   }
   __syncthreads();
   TSF_PACC(sm, PS_GATHER);
@@ -438,8 +602,13 @@ __device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, 
     double2 z[C];
 #pragma unroll
     for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
+    if (g.ctw) {
 #pragma unroll
-    for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], g.ctw[q * ncol + col]);
+    } else {
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+    }
     fft_reg<C, false>(z);
 #pragma unroll
     for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
@@ -456,7 +625,7 @@ __device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, 
       double2 &zb = B[(C - 1 - k2) * ncol + 2 * i + 1];
       double2 a = za, b = zb;
       pair_apply<DIV>(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
-                      tw[bin * g.tw2L], op.scale);
+                      op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
       za = a;
       zb = b;
     } else {
@@ -465,15 +634,16 @@ __device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, 
       if (k2 <= C / 2) {
         const int bin = g.L1 * k2;
         const double2 la = op.get(k2, 0, 0, bin);
+        const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
         double2 &za = B[k2 * ncol];
         if (kk == k2) {
           double2 a = za;
-          pair_self<DIV>(a, la, k2 == 0 ? op.nyquist(g.L) : la, tw[bin * g.tw2L], op.scale);
+          pair_self<DIV>(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
           za = a;
         } else {
           double2 &zb = B[kk * ncol];
           double2 a = za, b = zb;
-          pair_apply<DIV>(a, b, la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+          pair_apply<DIV>(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
           za = a;
           zb = b;
         }
@@ -483,15 +653,16 @@ __device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, 
       if (k2 < (C + 1) / 2) {
         const int bin = g.L1 / 2 + g.L1 * k2;
         const double2 la = op.get(k2, 1, 0, bin);
+        const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
         double2 &za = B[k2 * ncol + 1];
         if (km == k2) {
           double2 a = za;
-          pair_self<DIV>(a, la, la, tw[bin * g.tw2L], op.scale);
+          pair_self<DIV>(a, la, la, w, op.scale);
           za = a;
         } else {
           double2 &zb = B[km * ncol + 1];
           double2 a = za, b = zb;
-          pair_apply<DIV>(a, b, la, op.get(km, 1, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+          pair_apply<DIV>(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
           za = a;
           zb = b;
         }
@@ -506,17 +677,22 @@ __device__ __noinline__ void cross_staged(double2 *A, double2 *B, const Geo &g, 
 #pragma unroll
     for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
     fft_reg<C, true>(z);
+    if (g.ctw) {
 #pragma unroll
-    for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], g.ctw[q * ncol + col]);
+    } else {
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+    }
 #pragma unroll
     for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
   }
+  __syncthreads();
   TSF_PACC(sm, PS_COLI);
-  csync<C>();                    // every gather of A done before any scatter overwrites it
-  TSF_PACC(sm, PS_BAR2);
-  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM scatter
+#pragma unroll 4
+  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM scatter into O
     const int q = u / ncol, col = u - q * ncol;
-    remote<C>(A, uint32_t(q))[g.slot[col_k1(g.L1, C, r, col)]] = B[u];
+    remote<C>(O, uint32_t(q))[pidx(g.slot[col_k1(g.L1, C, r, col)])] = B[u];
   }
   TSF_PACC(sm, PS_SCATTER);
   csync<C>();                    // scatters landed
@@ -536,8 +712,8 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
   const int k1b = pseudo ? g.L1 / 2 : g.L1 - pi;
   int sa = 0, sb = 0;
   if (act) {
-    sa = g.slot[k1a];
-    sb = g.slot[k1b];
+    sa = pidx(g.slot[k1a]);
+    sb = pidx(g.slot[k1b]);
 #pragma unroll
     for (int q = 0; q < C; ++q) {
       const double2 *Aq = remote<C>(A, uint32_t(q));
@@ -601,13 +777,15 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
 }
 
 // y = op(x) for the CTA's local data already in A[0..L1) (natural order, visible).
-// On return A[0..L1) holds this CTA's part of the result (natural order, visible).
-template <int C, bool DIV>
-__device__ __noinline__ void apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
-                                   const double2 *__restrict__ tw, uint32_t r) {
+// Returns the buffer that holds this CTA's part of the result (natural order, visible):
+// O in the staged mode, A otherwise.  The caller writes the next input into A.
+template <int C, bool DIV, bool STG>
+__device__ __forceinline__ double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                          const double2 *__restrict__ tw, uint32_t r) {
   TSF_PT0();
   local_fft<false>(sm.A, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_F);
+  double2 *Y = sm.A;
   if constexpr (C == 1) {
     pointwise_local<DIV>(sm.A, g, op, tw);
     __syncthreads();
@@ -615,30 +793,37 @@ __device__ __noinline__ void apply(const Smem &sm, int L1e, const Geo &g, const 
   } else {
     csync<C>();                  // every local transform done before remote gathers
     TSF_PACC(sm, PS_BAR1);
-    if (sm.B) cross_staged<C, DIV>(sm.A, sm.B, g, op, tw, r, sm);
-    else cross_reg<C, DIV>(sm.A, g, op, tw, r);
+    if constexpr (STG) {
+      cross_staged<C, DIV>(sm.A, sm.B, sm.O, g, op, tw, r, sm);
+      Y = sm.O;
+    } else {
+      cross_reg<C, DIV>(sm.A, g, op, tw, r);
+    }
     TSF_PACC(sm, PS_BAR3);
   }
-  local_fft<true>(sm.A, g.L1, sm, L1e);
+  local_fft<true>(Y, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == 0) sm.prof[PS_APPLIES] += 1;
 #endif
+  return Y;
 }
 
 // ------------------------------------------------------------------------ operator setup
 enum Which { OP_A = 0, OP_B = 1, OP_AT = 2, OP_PINV = 3, OP_PTINV = 4 };
 
-__device__ __forceinline__ Geo geo_embed(const DevParams &P) {
+__device__ __forceinline__ Geo geo_embed(const DevParams &P, const Smem &sm) {
   Geo g;
   g.L1 = P.L1e; g.L = int(P.n); g.np = P.npe; g.twL = P.twN / int(P.n); g.tw2L = P.twN / int(2 * P.n);
   g.slot = P.slot_e;
+  g.ctw = sm.ctwe;
   return g;
 }
-__device__ __forceinline__ Geo geo_prec(const DevParams &P) {
+__device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
   Geo g;
   g.L1 = P.L1p; g.L = int(P.n / 2); g.np = P.npp; g.twL = P.twN / int(P.n / 2); g.tw2L = P.twN / int(P.n);
   g.slot = P.slot_p;
+  g.ctw = sm.ctwp;
   return g;
 }
 
@@ -646,24 +831,31 @@ __device__ __forceinline__ Geo geo_prec(const DevParams &P) {
 // preconditioner spectrum.  A = eta I - sigma L_j, B = eta I + (1-sigma) L_j (eq3.3), P the
 // circulant of (preku) with s(.) replaced by the chosen circulant approximation.
 __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int64_t j, int which,
-                                          uint32_t r) {
+                                          uint32_t r, const Smem &sm) {
   const double *lv = I.lev + 4 * j;
   const double eta = lv[0], c = lv[1], p = lv[2], q = lv[3];
   const double sigma = I.par[0];
   SpecOp op;
-  op.rC = int(r) * P.C;
+  const bool res = sm.lame != nullptr;
+  op.rC = res ? 0 : int(r) * P.C;
   op.eta = eta;
   op.ppq = p + q;
   op.pmq = p - q;
   if (which <= OP_AT) {
-    op.lam = I.lwe; op.sq = P.sq_e; op.np = P.npe; op.nyq = I.lwe[P.n];
+    op.lam = res ? sm.lame : I.lwe;
+    op.sq = res ? sm.sqe : P.sq_e;
+    op.pw = res ? sm.pwe : nullptr;
+    op.np = P.npe; op.nyq = I.lwe[P.n];
     op.mu = (which == OP_B) ? (1.0 - sigma) : -sigma;
     op.c2 = 2.0 * c;
     op.qcorr = 0.0;
     op.scale = P.scale_e;
     op.conj = (which == OP_AT);
   } else {
-    op.lam = I.lwp; op.sq = P.sq_p; op.np = P.npp; op.nyq = I.lwp[P.n / 2];
+    op.lam = res ? sm.lamp : I.lwp;
+    op.sq = res ? sm.sqp : P.sq_p;
+    op.pw = res ? sm.pwp : nullptr;
+    op.np = P.npp; op.nyq = I.lwp[P.n / 2];
     op.mu = -sigma;
     op.c2 = 2.0 * c * P.qscale_p;
     op.qcorr = P.strang ? -q * I.par[2] : 0.0;   // Strang s(W^T) midpoint fix (R-strang)
@@ -706,25 +898,25 @@ __device__ __forceinline__ void bind(VecT<VPT> &v, double *base, int64_t n, int 
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
 // Returns the local partial ||g||^2; g is left in A[0..npc) (and A[npc..2npc) is zero).
-template <int C, int VPT>
+template <int C, int VPT, bool STG>
 __device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
                                             uint32_t r, VecT<VPT> &U) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   for_elems<VPT>(npc, [&](int q, int e) {
-    sm.A[e] = U(q, e);
-    sm.A[e + npc] = zero2();
+    sm.A[pidx(e)] = U(q, e);
+    sm.A[pidx(e + npc)] = zero2();
   });
   __syncthreads();
-  const SpecOp opB = make_op(P, I, j, OP_B, r);
-  apply<C, false>(sm, P.L1e, geo_embed(P), opB, tw, r);
+  const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
+  const double2 *Y = apply<C, false, STG>(sm, P.L1e, geo_embed(P, sm), opB, tw, r);
   const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
   const int64_t hstride = n / 2;  // double2 per history row
   double acc = 0.0;
   TSF_PT0();
   for_elems<VPT>(npc, [&](int, int e) {
-    double2 g = sm.A[e];
+    double2 g = Y[pidx(e)];
     if (j >= 1) {
       double2 h0 = cscale(H[e], I.hwe[j]);
       double2 h1 = zero2(), h2 = h1, h3 = h1;
@@ -747,8 +939,8 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, i
       const double2 *F = reinterpret_cast<const double2 *>(I.ftab) + r * npc;
       g = cadd(g, F[j * hstride + e]);
     }
-    sm.A[e] = g;
-    sm.A[e + npc] = zero2();
+    sm.A[pidx(e)] = g;
+    sm.A[pidx(e + npc)] = zero2();
     acc += cdot(g, g);
   });
   TSF_PACC(sm, PS_RHS_HIST);
@@ -757,14 +949,14 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, i
 
 // ------------------------------------------------------------------------ one level
 // All control flow is uniform over the cluster (every CTA reduces to identical scalars).
-template <int C, int METHOD, int VPT>
+template <int C, int METHOD, int VPT, bool STG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
                                             uint32_t r, VecT<VPT> &U) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
-  const Geo ge = geo_embed(P), gp = geo_prec(P);
+  const Geo ge = geo_embed(P, sm), gp = geo_prec(P, sm);
   VecT<VPT> X, R, RH, PV, VV, S, PH, SH;
   if constexpr (VPT == 0) {
     const int off = int(r) * npc;
@@ -777,9 +969,9 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
   const long long tlev0 = clock64();
 #endif
 
-  double g2[1] = {rhs_phase<C, VPT>(P, I, j, sm, r, U)};
+  double g2[1] = {rhs_phase<C, VPT, STG>(P, I, j, sm, r, U)};
   for_elems<VPT>(npc, [&](int q, int e) {
-    const double2 g = sm.A[e];
+    const double2 g = sm.A[pidx(e)];
     R(q, e) = g;
     if (METHOD == TSF_BICGSTAB) { RH(q, e) = g; PV(q, e) = g; }
     X(q, e) = zero2();
@@ -789,8 +981,9 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
   const double rn0 = sqrt(rr0);
   int hs = 0, status = TSF_LEVEL_OK;
   double relres = 0.0;
-  const SpecOp opA = make_op(P, I, j, OP_A, r);
-  const SpecOp opP = make_op(P, I, j, OP_PINV, r);
+  const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
+  const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
+  const double2 *Y = sm.A;      // output buffer of the last operator application
 
   if (rr0 > 0.0 && METHOD == TSF_BICGSTAB) {
     double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
@@ -803,19 +996,21 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
           pv = caxpy(beta, caxpy(-omega, VV(q, e), PV(q, e)), R(q, e));
           PV(q, e) = pv;
         }
-        sm.A[e] = pv;
+        sm.A[pidx(e)] = pv;
       });
       __syncthreads();
-      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
       for_elems<VPT>(npc, [&](int q, int e) {
-        PH(q, e) = sm.A[e];
-        sm.A[e + npc] = zero2();
+        const double2 ph = Y[pidx(e)];
+        PH(q, e) = ph;
+        sm.A[pidx(e)] = ph;
+        sm.A[pidx(e + npc)] = zero2();
       });
       __syncthreads();
-      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
       double d[1] = {0.0};
       for_elems<VPT>(npc, [&](int q, int e) {
-        const double2 v = sm.A[e];
+        const double2 v = Y[pidx(e)];
         VV(q, e) = v;
         d[0] += cdot(RH(q, e), v);
       });
@@ -827,7 +1022,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       for_elems<VPT>(npc, [&](int q, int e) {
         const double2 s = caxpy(-alpha, VV(q, e), R(q, e));
         S(q, e) = s;
-        sm.A[e] = s;
+        sm.A[pidx(e)] = s;
         ss[0] += cdot(s, s);
       });
       csum<C, 1>(ss, sm, par);
@@ -838,16 +1033,18 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
         break;
       }
       //          shat = P^{-1} s; t = A shat; t.s, t.t
-      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
       for_elems<VPT>(npc, [&](int q, int e) {
-        SH(q, e) = sm.A[e];
-        sm.A[e + npc] = zero2();
+        const double2 sh = Y[pidx(e)];
+        SH(q, e) = sh;
+        sm.A[pidx(e)] = sh;
+        sm.A[pidx(e + npc)] = zero2();
       });
       __syncthreads();
-      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
       double tt[2] = {0.0, 0.0};
       for_elems<VPT>(npc, [&](int q, int e) {
-        const double2 t = sm.A[e];
+        const double2 t = Y[pidx(e)];
         const double2 s = S(q, e);
         tt[0] += cdot(t, s);
         tt[1] += cdot(t, t);
@@ -859,7 +1056,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       double rr[2] = {0.0, 0.0};
       for_elems<VPT>(npc, [&](int q, int e) {
         X(q, e) = caxpy(omega, SH(q, e), caxpy(alpha, PH(q, e), X(q, e)));
-        const double2 rn = caxpy(-omega, sm.A[e], S(q, e));
+        const double2 rn = caxpy(-omega, Y[pidx(e)], S(q, e));
         R(q, e) = rn;
         rr[0] += cdot(RH(q, e), rn);
         rr[1] += cdot(rn, rn);
@@ -876,15 +1073,24 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
     }
   } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
     // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r, p = z.
-    const SpecOp opAT = make_op(P, I, j, OP_AT, r);
-    const SpecOp opPT = make_op(P, I, j, OP_PTINV, r);
+    const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
+    const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
+    // z = P^{-T} (A^T r): A^T on the padded input, then P^{-T} on its first npc values
+    auto ktrans = [&]() -> const double2 * {
+      const double2 *Z = apply<C, false, STG>(sm, P.L1e, ge, opAT, tw, r);
+      if (!prec) return Z;
+      if (Z != sm.A) {
+        for_elems<VPT>(npc, [&](int, int e) { sm.A[pidx(e)] = Z[pidx(e)]; });
+        __syncthreads();
+      }
+      return apply<C, true, STG>(sm, P.L1e, gp, opPT, tw, r);
+    };
     // A[0..npc) holds r = g and A[npc..) is zero (rhs_phase)
     __syncthreads();
-    apply<C, false>(sm, P.L1e, ge, opAT, tw, r);
-    if (prec) apply<C, true>(sm, P.L1e, gp, opPT, tw, r);
+    Y = ktrans();
     double gz[1] = {0.0};
     for_elems<VPT>(npc, [&](int q, int e) {
-      const double2 z = sm.A[e];
+      const double2 z = Y[pidx(e)];
       PV(q, e) = z;
       gz[0] += cdot(z, z);
     });
@@ -896,19 +1102,21 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       for_elems<VPT>(npc, [&](int q, int e) {
         double2 pv;
         if (it == 0) pv = PV(q, e);
-        else { pv = caxpy(beta, PV(q, e), sm.A[e]); PV(q, e) = pv; }
-        sm.A[e] = pv;
+        else { pv = caxpy(beta, PV(q, e), Y[pidx(e)]); PV(q, e) = pv; }
+        sm.A[pidx(e)] = pv;
       });
       __syncthreads();
-      if (prec) apply<C, true>(sm, P.L1e, gp, opP, tw, r);
+      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
       for_elems<VPT>(npc, [&](int q, int e) {
-        PH(q, e) = sm.A[e];
-        sm.A[e + npc] = zero2();
+        const double2 ph = Y[pidx(e)];
+        PH(q, e) = ph;
+        sm.A[pidx(e)] = ph;
+        sm.A[pidx(e + npc)] = zero2();
       });
       __syncthreads();
-      apply<C, false>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
       double qq[1] = {0.0};
-      for_elems<VPT>(npc, [&](int, int e) { qq[0] += cdot(sm.A[e], sm.A[e]); });
+      for_elems<VPT>(npc, [&](int, int e) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); });
       csum<C, 1>(qq, sm, par);
       if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       const double a = gam / qq[0];
@@ -916,10 +1124,10 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       double rl[1] = {0.0};
       for_elems<VPT>(npc, [&](int q, int e) {
         X(q, e) = caxpy(a, PH(q, e), X(q, e));
-        const double2 rn = caxpy(-a, sm.A[e], R(q, e));
+        const double2 rn = caxpy(-a, Y[pidx(e)], R(q, e));
         R(q, e) = rn;
-        sm.A[e] = rn;
-        sm.A[e + npc] = zero2();
+        sm.A[pidx(e)] = rn;
+        sm.A[pidx(e + npc)] = zero2();
         rl[0] += cdot(rn, rn);
       });
       csum<C, 1>(rl, sm, par);
@@ -928,10 +1136,9 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
       if (relres < P.tol) break;
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
-      apply<C, false>(sm, P.L1e, ge, opAT, tw, r);
-      if (prec) apply<C, true>(sm, P.L1e, gp, opPT, tw, r);
+      Y = ktrans();
       double zz[1] = {0.0};
-      for_elems<VPT>(npc, [&](int, int e) { zz[0] += cdot(sm.A[e], sm.A[e]); });
+      for_elems<VPT>(npc, [&](int, int e) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); });
       csum<C, 1>(zz, sm, par);
       beta = zz[0] / gam;
       gam = zz[0];
@@ -959,15 +1166,15 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
 }
 
 // ------------------------------------------------------------------------ kernels
-template <int C, int METHOD, int VPT>
+template <int C, int METHOD, int VPT, bool STG>
 __global__ void __launch_bounds__(kThreads, (C == 1 && VPT == 0) ? 2 : 1)
-    k_solve(DevParams P, int32_t nlev, int32_t staged) {
+    k_solve(DevParams P, int32_t nlev, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
-  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   VecT<VPT> U;
   double2 *Ug = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
@@ -975,55 +1182,55 @@ __global__ void __launch_bounds__(kThreads, (C == 1 && VPT == 0) ? 2 : 1)
   else U.p = Ug;
   __syncthreads();
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, VPT>(P, I, j, sm, r, U);
+  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, VPT, STG>(P, I, j, sm, r, U);
   if constexpr (VPT > 0) for_elems<VPT>(npc, [&](int q, int e) { Ug[e] = U(q, e); });
 }
 
 __global__ void k_advance(int64_t *level, int64_t by, int64_t M);
 
 // Debug: one operator application of instance b at level j: in/out are permuted chunks.
-template <int C>
-__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t staged, int b, int64_t j,
+template <int C, bool STG>
+__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t, int b, int64_t j,
                                                               int which, const double *in, double *out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
-  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   const double2 *X = reinterpret_cast<const double2 *>(in) + r * npc;
   double2 *Y = reinterpret_cast<double2 *>(out) + r * npc;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool embed = which <= OP_AT;
   for (int e = threadIdx.x; e < npc; e += kThreads) {
-    sm.A[e] = X[e];
-    if (embed) sm.A[e + npc] = zero2();
+    sm.A[pidx(e)] = X[e];
+    if (embed) sm.A[pidx(e + npc)] = zero2();
   }
   __syncthreads();
-  const SpecOp op = make_op(P, I, j, which, r);
-  if (embed) apply<C, false>(sm, P.L1e, geo_embed(P), op, tw, r);
-  else apply<C, true>(sm, P.L1e, geo_prec(P), op, tw, r);
-  for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = sm.A[e];
+  const SpecOp op = make_op(P, I, j, which, r, sm);
+  const double2 *Z = embed ? apply<C, false, STG>(sm, P.L1e, geo_embed(P, sm), op, tw, r)
+                           : apply<C, true, STG>(sm, P.L1e, geo_prec(P, sm), op, tw, r);
+  for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
 }
 
 // Debug: RHS of the current level for every instance into V_R.
-template <int C>
-__global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t staged) {
+template <int C, bool STG>
+__global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = smem_view(smem_raw, P.L1e, staged != 0, P.prof);
-  load_twiddles(sm, P.L1e, reinterpret_cast<const double2 *>(P.tw), P.twN);
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int64_t j = *P.level;
   const int npc = P.L1p;
   __syncthreads();
   if (j >= P.M) return;
   VecT<0> U;
   U.p = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
-  rhs_phase<C, 0>(P, I, j, sm, r, U);
+  rhs_phase<C, 0, STG>(P, I, j, sm, r, U);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
-  for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[e];
+  for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
 }
 
 // ------------------------------------------------------------------------ launch API
@@ -1060,28 +1267,37 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Staged exchange (STG) exists for C > 1 only; register-resident vectors (VPT > 0) are
+// planned only together with the staged exchange or C == 1.
+#define TSF_STG_OF(CC, pl) ((CC) > 1 && (pl).staged)
 #define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
   template <>                                                                                   \
   cudaError_t launch_solve_c<CC>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) { \
     const int g = pl.B * CC;                                                                    \
-    const int32_t stg = pl.staged;                                                              \
+    const int32_t z = 0;                                                                        \
+    constexpr bool S1 = (CC) > 1;                                                               \
     if (pl.method == TSF_BICGSTAB) {                                                            \
-      if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 1>, pl, g, st, dp, nlev, stg); \
-      if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 2>, pl, g, st, dp, nlev, stg); \
-      return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0>, pl, g, st, dp, nlev, stg);            \
+      if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 1, S1>, pl, g, st, dp, nlev, z); \
+      if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 2, S1>, pl, g, st, dp, nlev, z); \
+      if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0, S1>, pl, g, st, dp, nlev, z); \
+      return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0, false>, pl, g, st, dp, nlev, z);       \
     }                                                                                           \
-    if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_CGNR, 1>, pl, g, st, dp, nlev, stg); \
-    if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_CGNR, 2>, pl, g, st, dp, nlev, stg); \
-    return launch_cluster(k_solve<CC, TSF_CGNR, 0>, pl, g, st, dp, nlev, stg);                  \
+    if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_CGNR, 1, S1>, pl, g, st, dp, nlev, z); \
+    if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_CGNR, 2, S1>, pl, g, st, dp, nlev, z); \
+    if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_CGNR, 0, S1>, pl, g, st, dp, nlev, z); \
+    return launch_cluster(k_solve<CC, TSF_CGNR, 0, false>, pl, g, st, dp, nlev, z);             \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \
                                      int which, const double *in, double *out, cudaStream_t st) { \
-    return launch_cluster(k_debug_apply<CC>, pl, CC, st, dp, int32_t(pl.staged), b, j, which, in, out); \
+    if (TSF_STG_OF(CC, pl))                                                                     \
+      return launch_cluster(k_debug_apply<CC, true>, pl, CC, st, dp, int32_t(0), b, j, which, in, out); \
+    return launch_cluster(k_debug_apply<CC, false>, pl, CC, st, dp, int32_t(0), b, j, which, in, out); \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_rhs_c<CC>(const Plan &pl, const DevParams &dp, cudaStream_t st) {      \
-    return launch_cluster(k_debug_rhs<CC>, pl, pl.B * CC, st, dp, int32_t(pl.staged));          \
+    if (TSF_STG_OF(CC, pl)) return launch_cluster(k_debug_rhs<CC, true>, pl, pl.B * CC, st, dp, int32_t(0)); \
+    return launch_cluster(k_debug_rhs<CC, false>, pl, pl.B * CC, st, dp, int32_t(0));           \
   }
 
 }  // namespace tsf

@@ -99,7 +99,8 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
 static bool cluster_ok(int64_t n, int C) {
   if (n / C > kMaxLocal) return false;
   if (n < 4LL * C * C) return false;
-  if (C > 1 && n / (2LL * C * C) > kThreads) return false;
+  // C > 1: staged exchange (local length <= 4096) or one column-pair task per thread
+  if (C > 1 && n / C > 4096 && n / (2LL * C * C) > kThreads) return false;
   return true;
 }
 
@@ -144,11 +145,14 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   const int64_t npc = n / (2 * C);
   P.vpt = npc <= kThreads ? 1 : (npc <= 2 * kThreads ? 2 : 0);
   if (const char *ev = std::getenv("TSF_VPT")) P.vpt = std::atoi(ev);
-  // staged cross-CTA exchange when two local buffers fit (L1e <= 4096)
+  if (C > 1 && n / C > 4096) P.vpt = 0;  // register exchange path keeps vectors in HBM
+  // staged cross-CTA exchange when three local buffers fit (L1e <= 4096); constant tables
+  // resident in SMEM when they fit too (L1e <= 1024)
   P.staged = (C > 1 && P.L1e <= 4096) ? 1 : 0;
   if (const char *es = std::getenv("TSF_STAGED")) P.staged = (C > 1) ? std::atoi(es) : 0;
-  const int64_t thi = P.L1e >= 64 ? P.L1e / 64 : 1, tlo = P.L1e >= 64 ? 64 : P.L1e;
-  P.smem = int64_t(16) * P.L1e * (1 + P.staged) + 16 * (thi + tlo) + 8 * 48 + 64;
+  P.resident = (P.staged && P.L1e <= 1024) ? 1 : 0;
+  if (const char *er = std::getenv("TSF_RESIDENT")) P.resident = P.staged ? std::atoi(er) : 0;
+  P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident);
 
   // shared tables
   size_t o = 0;
@@ -280,6 +284,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.n = pl.n; d.M = pl.M; d.B = pl.B; d.C = pl.C; d.K = pl.K; d.src_kind = pl.src_kind;
   d.method = pl.method; d.precond = pl.precond; d.maxit = pl.maxit;
   d.L1e = pl.L1e; d.L1p = pl.L1p; d.npe = pl.npe; d.npp = pl.npp;
+  d.staged = pl.staged; d.resident = pl.resident;
   d.tol = pl.tol;
   d.scale_e = 1.0 / (4.0 * double(pl.n));
   d.scale_p = 1.0 / (4.0 * double(pl.n / 2));

@@ -26,6 +26,7 @@ struct DevParams {
   int64_t n, M;
   int32_t B, C, K, src_kind, method, precond, maxit;
   int32_t L1e, L1p, npe, npp;      // local FFT lengths and column-pair tasks per CTA
+  int32_t staged, resident;        // exchange / SMEM-table modes (see Plan)
   double tol;
   double scale_e, scale_p;         // 1/(4L) folding of the real-FFT split and 1/L
   double qscale_p;                 // Lambda_Q scale of the preconditioner: 1 or (n-1)/n
@@ -51,7 +52,8 @@ struct Plan {
   double tol = 0;
   int32_t L1e = 0, L1p = 0, npe = 0, npp = 0;
   int32_t vpt = 0;      // Krylov vectors in registers: complex values per thread (0 = global)
-  int32_t staged = 0;   // cross-CTA step staged through a second SMEM buffer
+  int32_t staged = 0;   // cross-CTA step staged through SMEM buffers B (staging) and O (output)
+  int32_t resident = 0; // per-instance constant tables cached in SMEM (small local length)
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
@@ -113,5 +115,19 @@ TSF_HD inline int64_t perm_pos(int64_t n, int C, int64_t e) {
 }
 
 DevParams dev_params(const Plan &pl, char *ws);
+
+// Shared-memory carve-up of the solve kernel (must match smem_view in tsf_kernels.cuh):
+// A [L1e], B [L1e] and O [L1e] if staged, twiddles (direct [L1e] if resident, else two-level
+// [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], base spectra [L1e + L1p],
+// pair twiddles [L1e + L1p] (double2) and sine tables [L1e + L1p] (double); 48 doubles of
+// reduction scratch.
+TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident) {
+  const int64_t L1pad = L1e + L1e / 16;           // padded transform buffers (pidx)
+  int64_t c2 = staged ? (2 * L1pad + L1e) : L1pad;
+  if (resident) c2 += L1e + 3 * (L1e + L1p);
+  else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
+  int64_t d = 48 + (resident ? (L1e + L1p) : 0);
+  return 16 * c2 + 8 * d + 64;
+}
 
 }  // namespace tsf

@@ -9,9 +9,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# TSF_LIB_VARIANT=prof selects the section-timer build (developer profiling only)
-LIB_PATH = os.path.join(HERE, "lib", "libtsf_prof.so" if os.environ.get("TSF_LIB_VARIANT") == "prof"
-                        else "libtsf.so")
+# TSF_LIB_VARIANT=<name> selects a developer build lib/libtsf_<name>.so (e.g. "prof", the
+# section-timer build); unset = the product library
+_VARIANT = os.environ.get("TSF_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, "lib", f"libtsf_{_VARIANT}.so" if _VARIANT else "libtsf.so")
 
 TSF_OK = 0
 TSF_W_MAXIT = 1

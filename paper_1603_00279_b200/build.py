@@ -30,23 +30,29 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, verbose: bool, profile: bool = False) -> str:
-    obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ("_prof.o" if profile else ".o"))
-    cmd = [NVCC, *FLAGS, *(["-DTSF_PROFILE"] if profile else []), "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, verbose: bool, profile: bool = False, extra=(), variant: str = "") -> str:
+    tag = ("_prof" if profile else "") + (f"_{variant}" if variant else "")
+    obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + tag + ".o")
+    cmd = [NVCC, *FLAGS, *(["-DTSF_PROFILE"] if profile else []), *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    """Build libtsf.so (or the section-timer variant libtsf_prof.so with profile=True)."""
+def build(force: bool = False, verbose: bool = False, profile: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
+    """Build libtsf.so (or the section-timer variant libtsf_prof.so with profile=True, or a
+    developer variant libtsf_<variant>.so compiled with extra -D defines)."""
     lib = PROF_LIB if profile else LIB
+    if variant:
+        lib = os.path.join(LIBDIR, f"libtsf_{variant}.so")
     if not force and not _stale(lib):
         return lib
     os.makedirs(LIBDIR, exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose, profile), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, verbose, profile, extra, variant), SOURCES))
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs])
     os.replace(lib + ".tmp", lib)
     return lib

@@ -205,7 +205,7 @@ __global__ void k_set_level(int64_t *level, int64_t v) {
 
 __global__ void k_dbg_fft(double2 *buf, int L, const double2 *tw, int twN, int inverse) {
   extern __shared__ __align__(16) unsigned char raw[];
-  const Smem sm = smem_view(raw, L, L / 2, false, false, nullptr);
+  const Smem sm = smem_view(raw, L, L / 2, false, false, false, nullptr);
   const int f = twN / L;
   for (int i = threadIdx.x; i < tw_lo_len(L); i += blockDim.x) sm.tlo[i] = tw[i * f];
   for (int i = threadIdx.x; i < tw_hi_len(L); i += blockDim.x) sm.thi[i] = tw[(i << 6) * f];
@@ -226,7 +226,7 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
     if (idx <= n && lamA) {
       const Smem none = {};
       SpecOp op = make_op(P, I, j, OP_A, 0, none);
-      if (idx == n) { lamA[n] = op.nyquist(int(n)); continue; }
+      if (idx == n) { lamA[n] = op.nyquist_lam(int(n)); continue; }
       const int np = P.npe;
       const int i = int(idx % np), ab = int((idx / np) % 2), k2 = int((idx / (2 * np)) % C);
       const int r = int(idx / (2 * np * C));
@@ -236,7 +236,7 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
       const int64_t q = idx - n - 1;
       const Smem none = {};
       SpecOp op = make_op(P, I, j, OP_PINV, 0, none);
-      if (q == n / 2) { lamP[n / 2] = op.nyquist(int(n / 2)); continue; }
+      if (q == n / 2) { lamP[n / 2] = op.nyquist_lam(int(n / 2)); continue; }
       const int np = P.npp;
       const int i = int(q % np), ab = int((q / np) % 2), k2 = int((q / (2 * np)) % C);
       const int r = int(q / (2 * np * C));

@@ -28,6 +28,12 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef TSF_C1_BLOCKS
+#define TSF_C1_BLOCKS 2   // resident CTAs per SM of single-CTA instances
+#endif
+#ifndef TSF_BATCH
+#define TSF_BATCH 1       // elements per thread per batch of the HBM vector loops
+#endif
 namespace tsf {
 
 // ------------------------------------------------------------------------ complex helpers
@@ -99,6 +105,53 @@ __device__ __forceinline__ T *remote(T *p, uint32_t q) {
   else return cg::this_cluster().map_shared_rank(p, q);
 }
 
+// ------------------------------------------------------------------------ async DSMEM push
+// Cross-CTA data moves are pushes: the producer writes straight into the consumer's shared
+// memory with st.async, which signals the consumer's mbarrier with the byte count; the consumer
+// waits on its own mbarrier only.  No cluster-wide barrier, no GPU-scope fence (measured on
+// B200: cluster.sync ~390 cycles + MEMBAR.ALL.GPU; a 16 KB all-to-all push ~1.4k cycles vs ~2.6k
+// for pull-after-cluster.sync).  Buffers are reused only after a causal chain of exchanges
+// (DESIGN.md "Exchange protocol"), so no extra barrier protects them.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *m, uint32_t bytes) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smem_u32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p; TSF_W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra TSF_W; }" ::"r"(
+          smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+// 16-byte push of v to the shared::cluster address dst, completing 16 bytes on mbarrier mb
+__device__ __forceinline__ void push2(uint32_t dst, double2 v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "d"(v.x), "d"(v.y), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void push1(uint32_t dst, double v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v),
+               "r"(mb)
+               : "memory");
+}
+// Exchange state of one CTA: counts of operator exchanges and reductions so far (identical in
+// every thread of the cluster, since control flow is uniform); they select mbarrier phases.
+struct Xch {
+  uint32_t nap = 0, ncs = 0;
+};
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -116,7 +169,11 @@ struct Smem {
   double2 *ctwe, *ctwp;              // column twiddles (resident)
   double2 *lame, *lamp, *pwe, *pwp;  // base spectra / pair twiddles (resident)
   double *sqe, *sqp;                 // sine tables (resident)
+  double2 *vs;                       // Krylov vectors of this CTA's chunk (kSmemVec x L1p), or null
   double *wred, *cred;
+  double *red;                       // push reductions: [2][16][4] CTA partials (double-buffered)
+  uint64_t *mbar;                    // mbarriers: [0] exchange-in B, [1] exchange-back O, [2..3] red
+  int fuse_min;                      // local FFTs of at least this length use radix-16 passes
   unsigned long long *prof;
 };
 
@@ -125,6 +182,7 @@ struct Smem {
 // that ends with it.
 #ifdef TSF_PROFILE
 #define TSF_PT0() long long tsf_pt_ = clock64()
+#define TSF_PTR() tsf_pt_ = clock64()
 #define TSF_PACC(sm, slot)                                                                    \
   do {                                                                                      \
     const long long t_ = clock64();                                                         \
@@ -133,6 +191,7 @@ struct Smem {
   } while (0)
 #else
 #define TSF_PT0() do {} while (0)
+#define TSF_PTR() do {} while (0)
 #define TSF_PACC(sm, slot) do {} while (0)
 #endif
 enum ProfSlot { PS_FFT_F = 0, PS_BAR1, PS_GATHER, PS_COLF, PS_PAIRS, PS_COLI, PS_BAR2, PS_SCATTER,
@@ -141,13 +200,14 @@ __device__ __forceinline__ int tw_hi_len(int L1e) { return L1e >= 64 ? L1e / 64 
 __device__ __forceinline__ int tw_lo_len(int L1e) { return L1e >= 64 ? 64 : L1e; }
 
 __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, bool staged,
-                                          bool resident, unsigned long long *prof) {
+                                          bool resident, bool vsmem, unsigned long long *prof,
+                                          int fuse_min = 16 * kThreads) {
   Smem s = {};
   s.prof = prof;
+  s.fuse_min = fuse_min;
   double2 *c = reinterpret_cast<double2 *>(raw);
-  const int L1pad = L1e + L1e / 16;
-  s.A = c; c += L1pad;
-  if (staged) { s.B = c; c += L1e; s.O = c; c += L1pad; }
+  s.A = c; c += L1e;
+  if (staged) { s.B = c; c += L1e; s.O = c; c += L1e; }
   if (resident) {
     s.twd = c; c += L1e;
     s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
@@ -157,10 +217,13 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
     s.thi = c; c += tw_hi_len(L1e);
     s.tlo = c; c += tw_lo_len(L1e);
   }
+  if (vsmem) { s.vs = c; c += kSmemVec * L1p; }
   double *d = reinterpret_cast<double *>(c);
   if (resident) { s.sqe = d; d += L1e; s.sqp = d; d += L1p; }
   s.wred = d;
   s.cred = d + 40;
+  s.red = d + 48;
+  s.mbar = reinterpret_cast<uint64_t *>(d + 48 + 128);
   return s;
 }
 
@@ -215,48 +278,99 @@ __device__ __forceinline__ void load_constants(const DevParams &P, const double2
 }
 
 // Deterministic cluster-wide sum of NV <= 4 scalars: warp butterflies (exactly commutative,
-// so every lane holds the same bits) -> 8 warps in order -> C CTA partials through a
-// 32-lane butterfly in warp 0 (lanes >= C add 0) -> broadcast.
+// so every lane holds the same bits) -> 8 warps in order -> CTA partial; for C > 1 warp 0 pushes
+// the partial to every CTA of the cluster (slot red[par][r]) and every CTA adds the C partials
+// in rank order after its mbarrier completes -> identical bits in every CTA.
 template <int C, int NV>
-__device__ __forceinline__ void csum(double (&v)[NV], const Smem &sm, int &par) {
+__device__ __forceinline__ void csum(double (&v)[NV], const Smem &sm, Xch &xs) {
   TSF_PT0();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  const int par = int(xs.ncs & 1);
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) sm.wred[warp * 4 + k] = v[k];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) s += sm.wred[w * 4 + k];
-      sm.cred[par * 4 + k] = s;
-    }
-  }
   if constexpr (C == 1) {
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = sm.cred[par * 4 + k];
-  } else {
-    csync<C>();
-    if (warp == 0) {
+    if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        double s = lane < C ? remote<C>(sm.cred, uint32_t(lane))[par * 4 + k] : 0.0;
-        s = warp_sum(s);
-        if (lane == 0) sm.wred[32 + k] = s;
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) s += sm.wred[w * 4 + k];
+        sm.cred[par * 4 + k] = s;
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = sm.wred[32 + k];
+    for (int k = 0; k < NV; ++k) v[k] = sm.cred[par * 4 + k];
+  } else {
+    double *red = sm.red + par * 64;
+    uint64_t *mb = sm.mbar + 2 + par;
+    if (warp == 0) {
+      if (lane == 0) mbar_expect(mb, uint32_t(C * NV * 8));
+      if (lane < C) {
+        double s[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          s[k] = 0.0;
+#pragma unroll
+          for (int w = 0; w < kThreads / 32; ++w) s[k] += sm.wred[w * 4 + k];
+        }
+        const uint32_t r = crank<C>();
+        const uint32_t dst = mapa_u32(smem_u32(red + r * 4), uint32_t(lane));
+        const uint32_t mbr = mapa_u32(smem_u32(mb), uint32_t(lane));
+        if constexpr (NV == 1) push1(dst, s[0], mbr);
+        else {
+#pragma unroll
+          for (int k = 0; k + 1 < NV; k += 2) push2(dst + 8 * k, make_double2(s[k], s[k + 1]), mbr);
+          if constexpr (NV & 1) push1(dst + 8 * (NV - 1), s[NV - 1], mbr);
+        }
+      }
+    }
+    mbar_wait(mb, (xs.ncs >> 1) & 1);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < C; ++q) s += red[q * 4 + k];
+      v[k] = s;
+    }
   }
-  par ^= 1;
+  xs.ncs += 1;
   TSF_PACC(sm, PS_CSUM);
+}
+
+// mbarrier setup of a cluster kernel (before any push): init, make it visible cluster-wide.
+template <int C>
+__device__ __forceinline__ void xinit(const Smem &sm) {
+  if constexpr (C > 1) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 4; ++i) mbar_init(sm.mbar + i, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    csync<C>();
+  }
+}
+
+// Digit-reversal maps of the local FFT plan (DESIGN.md R-fft) in closed form, l = log2(L1):
+// slot p of the forward (DIF) output holds bin dperm(p); bin k sits in slot dslot(k).
+__device__ __forceinline__ uint32_t rev4(uint32_t x, int m) {   // reverse m base-4 digits
+  if (m == 0) return 0;
+  uint32_t y = __brev(x) >> (32 - 2 * m);
+  return ((y & 0x55555555u) << 1) | ((y >> 1) & 0x55555555u);
+}
+__device__ __forceinline__ int dperm(int p, int l) {
+  const int s4 = l >> 1;
+  if (!(l & 1)) return int(rev4(uint32_t(p), s4));
+  return int(2 * rev4(uint32_t(p) & ((1u << (2 * s4)) - 1), s4) + (uint32_t(p) >> (2 * s4)));
+}
+__device__ __forceinline__ int dslot(int k, int l) {
+  const int s4 = l >> 1;
+  if (!(l & 1)) return int(rev4(uint32_t(k), s4));
+  return int(rev4(uint32_t(k) >> 1, s4) + ((uint32_t(k) & 1u) << (2 * s4)));
 }
 
 // ------------------------------------------------------------------------ local FFT (SMEM)
@@ -276,10 +390,13 @@ __device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, dou
   a3 = csub(t1, t3);
 }
 
-// Padded SMEM index of element p of a transform buffer (A, O): one pad slot per 16 elements
-// makes the stride-4 and stride-16 accesses of the early DIT / late DIF stages bank-conflict
-// free.  Buffers hold L1 + L1/16 complex values.
-__device__ __forceinline__ int pidx(int p) { return p + (p >> 4); }
+// Swizzled SMEM index of element p of a transform buffer (A, O): bits 0..2 of p XOR
+// (p>>2 ^ p>>5 ^ p>>9).  High bits are kept, so it permutes every aligned block of 8 and is a
+// bijection on every power-of-two range.  For 16-byte elements (8 lanes per wavefront) it
+// makes every radix-4 / radix-2 stage, every fused radix-16 pass and the linear loops free of
+// shared-memory bank conflicts, and keeps the digit-reversed pair reads <= ~2.3-way
+// (tools/smem_conflicts.py, L1 = 2^8..2^13).
+__device__ __forceinline__ int pidx(int p) { return p ^ (((p >> 2) ^ (p >> 5) ^ (p >> 9)) & 7); }
 
 // one stage: m = 2^lm, twiddle W_m^{kq} = W_{L1e}^{kq (L1e/m)}
 template <bool INV, int RADIX>
@@ -399,9 +516,9 @@ __device__ __forceinline__ void local_fft(double2 *A, int L1, const Smem &sm, in
   const int l = __ffs(L1) - 1;
   const int S4 = l >> 1;
   const bool r2 = l & 1;
-  // fuse only when every thread owns a 16-point super-butterfly (else radix-4 stages keep
-  // all threads busy); the data placement is the same either way
-  const bool fuse = L1 >= 16 * kThreads;
+  // fuse when the local length reaches sm.fuse_min (default: every thread owns a 16-point
+  // super-butterfly); the data placement is the same either way
+  const bool fuse = L1 >= sm.fuse_min && L1 >= 256;
   const int npair = fuse ? (S4 >> 1) : 0;   // fused pairs (2i+1, 2i), i < npair
   if (!fuse) {
     if (!INV) {
@@ -487,6 +604,13 @@ struct SpecOp {
   int rC;               // r * C (0 for resident slices)
   double eta, mu, ppq, pmq, c2, qcorr, scale;
   bool conj;
+  bool div;             // apply 1/lambda (circulant solve) instead of lambda
+  // multiplier of a bin: lambda, or 1/lambda = conj(lambda)/|lambda|^2 for a solve
+  __device__ __forceinline__ double2 eff(double2 l) const {
+    if (!div) return l;
+    const double inv = 1.0 / (l.x * l.x + l.y * l.y);
+    return make_double2(l.x * inv, -l.y * inv);
+  }
   // W_{2L}^{bin} of bin (k2, ab, i): resident table or the global twiddle table
   __device__ __forceinline__ double2 wtw(int k2, int ab, int i, int bin, const double2 *tw,
                                          int tw2L) const {
@@ -499,27 +623,31 @@ struct SpecOp {
     const double im = pmq * b.y + c2 * s;
     return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
   }
-  __device__ __forceinline__ double2 get(int k2, int ab, int i, int bin) const {
-    return lam_idx(((rC + k2) * 2 + ab) * np + i, bin);
+  // lam_idx for tables known to be in global memory (read-only path, freely reordered)
+  __device__ __forceinline__ double2 lam_idx_g(int idx, int bin) const {
+    const double2 b = __ldg(lam + idx);
+    const double s = __ldg(sq + idx);
+    const double re = ppq * b.x + ((bin & 1) ? -qcorr : qcorr);
+    const double im = pmq * b.y + c2 * s;
+    return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
   }
-  __device__ __forceinline__ double2 nyquist(int Lbin) const {
+  // effective multiplier (lambda or 1/lambda) of bin (k2, ab, i)
+  __device__ __forceinline__ double2 get(int k2, int ab, int i, int bin) const {
+    return eff(lam_idx(((rC + k2) * 2 + ab) * np + i, bin));
+  }
+  __device__ __forceinline__ double2 nyquist_lam(int Lbin) const {
     const double re = ppq * nyq.x + ((Lbin & 1) ? -qcorr : qcorr);
     const double im = pmq * nyq.y;
     return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
   }
+  __device__ __forceinline__ double2 nyquist(int Lbin) const { return eff(nyquist_lam(Lbin)); }
 };
 
-__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
-  const double d = b.x * b.x + b.y * b.y;
-  const double inv = 1.0 / d;
-  return make_double2((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
-}
-
 // Real-FFT split for the pair of bins (k, L-k) of a length-L complex transform z of a
-// 2L-point real sequence x (z_m = x_{2m} + i x_{2m+1}), apply Y = X * lambda (or X / lambda)
-// to X_k and X_{L-k}, and merge back to Z' such that the unnormalized inverse DFT of Z'
-// returns y packed the same way.  w = exp(-i pi k / L); s = 1/(4L) folds the halves and 1/L.
-template <bool DIV>
+// 2L-point real sequence x (z_m = x_{2m} + i x_{2m+1}), apply Y = X * la (bin k) and
+// Y = X * lb (bin L-k), la/lb the effective multipliers (lambda or 1/lambda), and merge back to
+// Z' such that the unnormalized inverse DFT of Z' returns y packed the same way.
+// w = exp(-i pi k / L); s = 1/(4L) folds the halves and 1/L.
 __device__ __forceinline__ void pair_apply(double2 &Za, double2 &Zb, double2 la, double2 lb,
                                            double2 w, double s) {
   const double2 cZb = cconj(Zb);
@@ -528,8 +656,8 @@ __device__ __forceinline__ void pair_apply(double2 &Za, double2 &Zb, double2 la,
   const double2 wO = cmul(w, Op);
   const double2 Xa = cadd(Ep, wO);                // 2 X_k
   const double2 Xb = cconj(csub(Ep, wO));         // 2 X_{L-k}
-  const double2 Ya = DIV ? cdiv(Xa, la) : cmul(Xa, la);
-  const double2 Yb = DIV ? cdiv(Xb, lb) : cmul(Xb, lb);
+  const double2 Ya = cmul(Xa, la);
+  const double2 Yb = cmul(Xb, lb);
   const double2 cYb = cconj(Yb);
   const double2 E2 = cadd(Ya, cYb);               // 4 E'_k
   const double2 O2 = cmulc(csub(Ya, cYb), w);     // 4 O'_k
@@ -537,37 +665,40 @@ __device__ __forceinline__ void pair_apply(double2 &Za, double2 &Zb, double2 la,
   Zb = cscale(cadd(cconj(E2), mul_i(cconj(O2))), s);
 }
 
-template <bool DIV>
 __device__ __forceinline__ void pair_self(double2 &Z, double2 la, double2 lb, double2 w, double s) {
   double2 a = Z, b = Z;
-  pair_apply<DIV>(a, b, la, lb, w, s);
+  pair_apply(a, b, la, lb, w, s);
   Z = a;
 }
 
 struct Geo {
   int L1, L, np, twL, tw2L;   // twL = twN/L (W_L factor), tw2L = twN/(2L)
+  int l1;                     // log2(L1)
   const int32_t *slot;
   const double2 *ctw;         // resident column twiddles W_L^{q k1(col)} [q ncol + col]
 };
 
-// C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).
-template <bool DIV>
+// C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).  The spectra and
+// twiddles are global (read-only path, so loads of later pairs overlap earlier arithmetic).
 __device__ __forceinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
                                              const double2 *__restrict__ tw) {
-  for (int i = threadIdx.x; i < g.np; i += kThreads) {
-    if (i == 0) {
-      const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
-      double2 a = A[sa], b = A[sb];
-      pair_self<DIV>(a, op.get(0, 0, 0, 0), op.nyquist(g.L), tw[0], op.scale);
-      const double2 lm = op.get(0, 1, 0, g.L / 2);
-      pair_self<DIV>(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
-      A[sa] = a; A[sb] = b;
-    } else {
-      const int sa = pidx(g.slot[i]), sb = pidx(g.slot[g.L1 - i]);
-      double2 a = A[sa], b = A[sb];
-      pair_apply<DIV>(a, b, op.get(0, 0, i, i), op.get(0, 1, i, g.L - i), tw[i * g.tw2L], op.scale);
-      A[sa] = a; A[sb] = b;
-    }
+  if (threadIdx.x == 0) {
+    const int sa = pidx(dslot(0, g.l1)), sb = pidx(dslot(g.L1 / 2, g.l1));
+    double2 a = A[sa], b = A[sb];
+    pair_self(a, op.eff(op.lam_idx_g(0, 0)), op.nyquist(g.L), __ldg(tw), op.scale);
+    const double2 lm = op.eff(op.lam_idx_g(g.np, g.L / 2));
+    pair_self(b, lm, lm, __ldg(tw + (g.L / 2) * g.tw2L), op.scale);
+    A[sa] = a; A[sb] = b;
+  }
+#pragma unroll 4
+  for (int i = threadIdx.x + 1; i < g.np; i += kThreads) {
+    const double2 la = op.eff(op.lam_idx_g(i, i));
+    const double2 lb = op.eff(op.lam_idx_g(g.np + i, g.L - i));
+    const double2 w = __ldg(tw + i * g.tw2L);
+    const int sa = pidx(dslot(i, g.l1)), sb = pidx(dslot(g.L1 - i, g.l1));
+    double2 a = A[sa], b = A[sb];
+    pair_apply(a, b, la, lb, w, op.scale);
+    A[sa] = a; A[sb] = b;
   }
 }
 
@@ -578,72 +709,90 @@ __device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col) {
   return (col & 1) ? L1 - pi : pi;
 }
 
-// C > 1, staged through the local buffer B (layout B[q * ncol + col], ncol = L1/C):
-//   gather A_q[slot(k1)] from every CTA -> per column: twiddle W_L^{q k1}, DFT_C -> per bin
-//   pair: spectral op -> per column: inverse DFT_C, conj twiddle -> scatter to O_{m2}.
-// The result lands in the output buffers O, so no CTA can still be gathering from the
-// buffer being written: two cluster barriers per application (before the gather, after the
-// scatter).
-template <int C, bool DIV>
-__device__ __forceinline__ void cross_staged(double2 *A, double2 *B, double2 *O, const Geo &g,
-                                          const SpecOp &op, const double2 *__restrict__ tw, uint32_t r,
-                                          const Smem &sm) {
+// C > 1, staged: the four-step column stage through the receive buffer B and the output O,
+// both filled by pushes.  B layout: B[q * ncol + ab * np + i]
+// holds row q (source CTA q, bin k1 + L1 k2 after the column DFT) of this CTA's column
+// (i, ab), k1 = col_k1(i, ab).  Steps: push the local DIF output (slot p holds bin dperm(p)) to
+// the owner of its column pair; column DFT_C with twiddles W_L^{q k1}; per bin pair the real
+// split + spectral op; inverse column DFT, conjugate twiddles, push row q back to CTA q's O at
+// the slot of k1.  Returns with O complete and visible.
+template <int C>
+__device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, const Geo &g,
+                                           const SpecOp &op, const double2 *__restrict__ tw, uint32_t r,
+                                           const Smem &sm, Xch &xs) {
   TSF_PT0();
-  const int ncol = g.L1 / C;
-#pragma unroll 4
-  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM gather
-    const int q = u / ncol, col = u - q * ncol;
-    B[u] = remote<C>(A, uint32_t(q))[pidx(g.slot[col_k1(g.L1, C, r, col)])];
+  const int L1 = g.L1, l1 = g.l1, ncol = L1 / C, np = g.np;
+  uint64_t *mbB = sm.mbar, *mbO = sm.mbar + 1;
+  const uint32_t ph = xs.nap & 1;
+  if (threadIdx.x == 0) {
+    mbar_expect(mbB, uint32_t(L1 * 16));
+    mbar_expect(mbO, uint32_t(L1 * 16));
   }
-  __syncthreads();
+  {
+    const uint32_t bB = smem_u32(B), aB = smem_u32(mbB);
+#pragma unroll 4
+    for (int p = threadIdx.x; p < L1; p += kThreads) {
+      const int k1 = dperm(p, l1);
+      int pi, ab;
+      if (k1 == 0) { pi = 0; ab = 0; }
+      else if (k1 == L1 / 2) { pi = 0; ab = 1; }
+      else if (k1 < L1 / 2) { pi = k1; ab = 0; }
+      else { pi = L1 - k1; ab = 1; }
+      const uint32_t q = uint32_t(pi) & (C - 1);
+      const int idx = int(r) * ncol + ab * np + pi / C;
+      push2(mapa_u32(bB + 16u * idx, q), A[pidx(p)], mapa_u32(aB, q));
+    }
+  }
+  mbar_wait(mbB, ph);
   TSF_PACC(sm, PS_GATHER);
-  for (int col = threadIdx.x; col < ncol; col += kThreads) {  // column DFT_C
-    const int k1 = col_k1(g.L1, C, r, col);
+  for (int t = threadIdx.x; t < ncol; t += kThreads) {        // column DFT_C
+    const int ab = t / np, i = t - ab * np, colo = 2 * i + ab;
+    const int k1 = col_k1(L1, C, r, colo);
     double2 z[C];
 #pragma unroll
-    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
+    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
     if (g.ctw) {
 #pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], g.ctw[q * ncol + col]);
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], g.ctw[q * ncol + colo]);
     } else {
 #pragma unroll
       for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
     }
     fft_reg<C, false>(z);
 #pragma unroll
-    for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
+    for (int q = 0; q < C; ++q) B[q * ncol + t] = z[q];
   }
   __syncthreads();
   TSF_PACC(sm, PS_COLF);
-  // bin pairs: item u = k2 * np + i; regular pair (col 2i row k2) <-> (col 2i+1 row C-1-k2)
-  for (int u = threadIdx.x; u < g.np * C; u += kThreads) {
-    const int k2 = u / g.np, i = u - k2 * g.np;
+  // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1))
+  for (int u = threadIdx.x; u < np * C; u += kThreads) {
+    const int k2 = u / np, i = u - k2 * np;
     const int pi = int(r) + i * C;
     if (pi != 0) {
-      const int bin = pi + g.L1 * k2;
-      double2 &za = B[k2 * ncol + 2 * i];
-      double2 &zb = B[(C - 1 - k2) * ncol + 2 * i + 1];
+      const int bin = pi + L1 * k2;
+      double2 &za = B[k2 * ncol + i];
+      double2 &zb = B[(C - 1 - k2) * ncol + np + i];
       double2 a = za, b = zb;
-      pair_apply<DIV>(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
-                      op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
+      pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
+                 op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
       za = a;
       zb = b;
     } else {
       // column 0 (bins L1 k2) pairs k2 <-> (C - k2) mod C; k2 = 0 pairs with the Nyquist bin
       const int kk = (C - k2) % C;
       if (k2 <= C / 2) {
-        const int bin = g.L1 * k2;
+        const int bin = L1 * k2;
         const double2 la = op.get(k2, 0, 0, bin);
         const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
         double2 &za = B[k2 * ncol];
         if (kk == k2) {
           double2 a = za;
-          pair_self<DIV>(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
+          pair_self(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
           za = a;
         } else {
           double2 &zb = B[kk * ncol];
           double2 a = za, b = zb;
-          pair_apply<DIV>(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
+          pair_apply(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
           za = a;
           zb = b;
         }
@@ -651,18 +800,18 @@ __device__ __forceinline__ void cross_staged(double2 *A, double2 *B, double2 *O,
       // column L1/2 (bins L1/2 + L1 k2) pairs k2 <-> C-1-k2
       const int km = C - 1 - k2;
       if (k2 < (C + 1) / 2) {
-        const int bin = g.L1 / 2 + g.L1 * k2;
+        const int bin = L1 / 2 + L1 * k2;
         const double2 la = op.get(k2, 1, 0, bin);
         const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
-        double2 &za = B[k2 * ncol + 1];
+        double2 &za = B[k2 * ncol + np];
         if (km == k2) {
           double2 a = za;
-          pair_self<DIV>(a, la, la, w, op.scale);
+          pair_self(a, la, la, w, op.scale);
           za = a;
         } else {
-          double2 &zb = B[km * ncol + 1];
+          double2 &zb = B[km * ncol + np];
           double2 a = za, b = zb;
-          pair_apply<DIV>(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
+          pair_apply(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
           za = a;
           zb = b;
         }
@@ -671,36 +820,36 @@ __device__ __forceinline__ void cross_staged(double2 *A, double2 *B, double2 *O,
   }
   __syncthreads();
   TSF_PACC(sm, PS_PAIRS);
-  for (int col = threadIdx.x; col < ncol; col += kThreads) {  // inverse column DFT_C
-    const int k1 = col_k1(g.L1, C, r, col);
-    double2 z[C];
+  {
+    const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
+    for (int t = threadIdx.x; t < ncol; t += kThreads) {      // inverse column DFT_C + push back
+      const int ab = t / np, i = t - ab * np, colo = 2 * i + ab;
+      const int k1 = col_k1(L1, C, r, colo);
+      double2 z[C];
 #pragma unroll
-    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + col];
-    fft_reg<C, true>(z);
-    if (g.ctw) {
+      for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
+      fft_reg<C, true>(z);
+      if (g.ctw) {
 #pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], g.ctw[q * ncol + col]);
-    } else {
+        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], g.ctw[q * ncol + colo]);
+      } else {
 #pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      }
+      const uint32_t dst = bO + 16u * uint32_t(pidx(dslot(k1, l1)));
+#pragma unroll
+      for (int q = 0; q < C; ++q) push2(mapa_u32(dst, uint32_t(q)), z[q], mapa_u32(aO, uint32_t(q)));
     }
-#pragma unroll
-    for (int q = 0; q < C; ++q) B[q * ncol + col] = z[q];
   }
-  __syncthreads();
   TSF_PACC(sm, PS_COLI);
-#pragma unroll 4
-  for (int u = threadIdx.x; u < g.L1; u += kThreads) {       // DSMEM scatter into O
-    const int q = u / ncol, col = u - q * ncol;
-    remote<C>(O, uint32_t(q))[pidx(g.slot[col_k1(g.L1, C, r, col)])] = B[u];
-  }
-  TSF_PACC(sm, PS_SCATTER);
-  csync<C>();                    // scatters landed
+  mbar_wait(mbO, ph);
+  xs.nap += 1;
+  TSF_PACC(sm, PS_BAR3);
 }
 
 // C > 1 without a staging buffer (shared memory full): one thread per column pair keeps the
 // 2C values in registers across the barrier.  Requires np <= kThreads.
-template <int C, bool DIV>
+template <int C>
 __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &op,
                                        const double2 *__restrict__ tw, uint32_t r) {
   double2 za[C], zb[C];
@@ -712,8 +861,8 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
   const int k1b = pseudo ? g.L1 / 2 : g.L1 - pi;
   int sa = 0, sb = 0;
   if (act) {
-    sa = pidx(g.slot[k1a]);
-    sb = pidx(g.slot[k1b]);
+    sa = pidx(dslot(k1a, g.l1));
+    sb = pidx(dslot(k1b, g.l1));
 #pragma unroll
     for (int q = 0; q < C; ++q) {
       const double2 *Aq = remote<C>(A, uint32_t(q));
@@ -731,7 +880,7 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
 #pragma unroll
       for (int k2 = 0; k2 < C; ++k2) {
         const int bin = k1a + g.L1 * k2;
-        pair_apply<DIV>(za[k2], zb[C - 1 - k2], op.get(k2, 0, i, bin),
+        pair_apply(za[k2], zb[C - 1 - k2], op.get(k2, 0, i, bin),
                         op.get(C - 1 - k2, 1, i, g.L - bin), tw[bin * g.tw2L], op.scale);
       }
     } else {
@@ -742,9 +891,9 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
         const double2 la = op.get(k2, 0, 0, bin);
         if (kk == k2) {
           const double2 lb = (k2 == 0) ? op.nyquist(g.L) : la;
-          pair_self<DIV>(za[k2], la, lb, tw[bin * g.tw2L], op.scale);
+          pair_self(za[k2], la, lb, tw[bin * g.tw2L], op.scale);
         } else {
-          pair_apply<DIV>(za[k2], za[kk], la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+          pair_apply(za[k2], za[kk], la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
         }
       }
 #pragma unroll
@@ -752,8 +901,8 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
         const int kk = C - 1 - k2;
         const int bin = g.L1 / 2 + g.L1 * k2;
         const double2 la = op.get(k2, 1, 0, bin);
-        if (kk == k2) pair_self<DIV>(zb[k2], la, la, tw[bin * g.tw2L], op.scale);
-        else pair_apply<DIV>(zb[k2], zb[kk], la, op.get(kk, 1, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+        if (kk == k2) pair_self(zb[k2], la, la, tw[bin * g.tw2L], op.scale);
+        else pair_apply(zb[k2], zb[kk], la, op.get(kk, 1, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
       }
     }
     fft_reg<C, true>(za);
@@ -779,27 +928,34 @@ __device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &o
 // y = op(x) for the CTA's local data already in A[0..L1) (natural order, visible).
 // Returns the buffer that holds this CTA's part of the result (natural order, visible):
 // O in the staged mode, A otherwise.  The caller writes the next input into A.
-template <int C, bool DIV, bool STG>
-__device__ __forceinline__ double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
-                                          const double2 *__restrict__ tw, uint32_t r) {
+// Inlined at each call site (a __noinline__ variant, -DTSF_APPLY_NOINLINE, shrinks the SASS
+// ~5x but measured 20% slower at C3: its arguments travel through the stack).
+#ifdef TSF_APPLY_NOINLINE
+#define TSF_APPLY_ATTR __noinline__
+#else
+#define TSF_APPLY_ATTR __forceinline__
+#endif
+template <int C, bool STG>
+__device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                       const double2 *__restrict__ tw, uint32_t r, Xch &xs) {
   TSF_PT0();
   local_fft<false>(sm.A, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_F);
   double2 *Y = sm.A;
   if constexpr (C == 1) {
-    pointwise_local<DIV>(sm.A, g, op, tw);
+    pointwise_local(sm.A, g, op, tw);
     __syncthreads();
     TSF_PACC(sm, PS_PAIRS);
   } else {
-    csync<C>();                  // every local transform done before remote gathers
-    TSF_PACC(sm, PS_BAR1);
     if constexpr (STG) {
-      cross_staged<C, DIV>(sm.A, sm.B, sm.O, g, op, tw, r, sm);
+      cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs);
       Y = sm.O;
     } else {
-      cross_reg<C, DIV>(sm.A, g, op, tw, r);
+      csync<C>();                // every local transform done before remote gathers
+      TSF_PACC(sm, PS_BAR1);
+      cross_reg<C>(sm.A, g, op, tw, r);
     }
-    TSF_PACC(sm, PS_BAR3);
+    TSF_PTR();
   }
   local_fft<true>(Y, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_I);
@@ -817,6 +973,7 @@ __device__ __forceinline__ Geo geo_embed(const DevParams &P, const Smem &sm) {
   g.L1 = P.L1e; g.L = int(P.n); g.np = P.npe; g.twL = P.twN / int(P.n); g.tw2L = P.twN / int(2 * P.n);
   g.slot = P.slot_e;
   g.ctw = sm.ctwe;
+  g.l1 = __ffs(g.L1) - 1;
   return g;
 }
 __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
@@ -824,6 +981,7 @@ __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
   g.L1 = P.L1p; g.L = int(P.n / 2); g.np = P.npp; g.twL = P.twN / int(P.n / 2); g.tw2L = P.twN / int(P.n);
   g.slot = P.slot_p;
   g.ctw = sm.ctwp;
+  g.l1 = __ffs(g.L1) - 1;
   return g;
 }
 
@@ -851,6 +1009,7 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
     op.qcorr = 0.0;
     op.scale = P.scale_e;
     op.conj = (which == OP_AT);
+    op.div = false;
   } else {
     op.lam = res ? sm.lamp : I.lwp;
     op.sq = res ? sm.sqp : P.sq_p;
@@ -861,61 +1020,110 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
     op.qcorr = P.strang ? -q * I.par[2] : 0.0;   // Strang s(W^T) midpoint fix (R-strang)
     op.scale = P.scale_p;
     op.conj = (which == OP_PTINV);
+    op.div = true;
   }
   return op;
 }
 
 // ------------------------------------------------------------------------ vector storage
-// VPT > 0: this thread's VPT complex elements e = tid + q T in registers; VPT == 0: global.
-template <int VPT>
-struct VecT {
-  double2 d[VPT > 0 ? VPT : 1];
-  double2 *p;
-  __device__ __forceinline__ double2 &operator()(int q, int e) {
-    if constexpr (VPT > 0) return d[q];
-    else return p[e];
-  }
+// Krylov vectors of this CTA's chunk (npc = L1p complex values): SMEM slots when the plan
+// keeps them on chip (P.vsmem), else the instance's HBM vector block (permuted chunks).
+// Every vector loop visits element e = tid + q T, so each element is only ever touched by
+// the same thread and vector updates need no barrier.
+struct Vecs {
+  double2 *U, *X, *R, *RH, *P, *V, *S, *PH, *SH;
 };
 
-template <int VPT, class F>
-__device__ __forceinline__ void for_elems(int npc, F &&f) {
-  if constexpr (VPT > 0) {
-#pragma unroll
-    for (int q = 0; q < VPT; ++q) {
-      const int e = threadIdx.x + q * kThreads;
-      if (e < npc) f(q, e);
-    }
+__device__ __forceinline__ Vecs vec_view(const DevParams &P, const Inst &I, const Smem &sm, uint32_t r) {
+  Vecs v;
+  const int npc = P.L1p;
+  auto g = [&](int slot) { return reinterpret_cast<double2 *>(I.vec + slot * P.n) + r * npc; };
+  if (sm.vs) {
+    double2 *b = sm.vs;
+    v.U = b; v.X = b + npc; v.R = b + 2 * npc; v.RH = b + 3 * npc; v.P = b + 4 * npc;
+    v.V = b + 5 * npc; v.S = b + 6 * npc; v.PH = b + 7 * npc; v.SH = b + 8 * npc;
   } else {
-    for (int e = threadIdx.x; e < npc; e += kThreads) f(0, e);
+    v.U = g(V_U); v.X = g(V_X); v.R = g(V_R); v.RH = g(V_RH); v.P = g(V_P);
+    v.V = g(V_V); v.S = g(V_S); v.PH = g(V_PH); v.SH = g(V_SH);
   }
+  return v;
 }
 
-template <int VPT>
-__device__ __forceinline__ void bind(VecT<VPT> &v, double *base, int64_t n, int slot, int off) {
-  v.p = reinterpret_cast<double2 *>(base + slot * n) + off;
+// Per-CTA context in shared memory: carve-up, instance view, vector pointers, transform
+// geometries and the level's five operators.  Kept in SMEM rather than registers: as register
+// values these ~160 words of bookkeeping stay live across a whole Krylov iteration and force
+// spills; from SMEM they are reloaded (LDS, broadcast) after every barrier instead.
+struct Ctx {
+  Smem sm;
+  Inst I;
+  Vecs V;
+  Geo ge, gp;
+  SpecOp op[5];
+};
+
+__device__ __forceinline__ void ctx_init(Ctx &ctx, const DevParams &P, unsigned char *raw, int b, uint32_t r) {
+  if (threadIdx.x == 0) {
+    ctx.I = inst_view(P, b);
+    ctx.sm = smem_view(raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+    ctx.V = vec_view(P, ctx.I, ctx.sm, r);
+    ctx.ge = geo_embed(P, ctx.sm);
+    ctx.gp = geo_prec(P, ctx.sm);
+  }
+  __syncthreads();
 }
+// level-j operators A, B, A^T, P^{-1}, P^{-T} into ctx.op (caller synchronizes)
+__device__ __forceinline__ void ctx_ops(Ctx &ctx, const DevParams &P, int64_t j, uint32_t r) {
+  if (threadIdx.x < 5) ctx.op[threadIdx.x] = make_op(P, ctx.I, j, int(threadIdx.x), r, ctx.sm);
+}
+
+#define TSF_FOR_E(npc) for (int e = threadIdx.x; e < (npc); e += kThreads)
+
+// Element loop in batches of U elements per thread: every load of the batch (ld) is issued
+// before any store (op), so HBM-resident vectors get U x (loads per element) requests in flight
+// per thread.  Elements are visited in the same per-thread order as TSF_FOR_E, so per-thread
+// partial sums (and therefore the reductions) are bit-identical to the unbatched loop.
+template <int U, class T, class LD, class OP>
+__device__ __forceinline__ void batched(int npc, LD &&ld, OP &&op) {
+  for (int e0 = threadIdx.x; e0 < npc; e0 += U * kThreads) {
+    T t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e < npc) ld(e, t[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e < npc) op(e, t[u]);
+    }
+  }
+}
+struct T1 { double2 a; };
+struct T2 { double2 a, b; };
+struct T3 { double2 a, b, c; };
+struct T5 { double2 a, b, c, d, f; };
 
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
 // Returns the local partial ||g||^2; g is left in A[0..npc) (and A[npc..2npc) is zero).
-template <int C, int VPT, bool STG>
-__device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
-                                            uint32_t r, VecT<VPT> &U) {
+template <int C, bool STG>
+__device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
+                                            const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
+                                            Xch &xs) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  for_elems<VPT>(npc, [&](int q, int e) {
-    sm.A[pidx(e)] = U(q, e);
+  TSF_FOR_E(npc) {
+    sm.A[pidx(e)] = U[e];
     sm.A[pidx(e + npc)] = zero2();
-  });
+  }
   __syncthreads();
-  const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
-  const double2 *Y = apply<C, false, STG>(sm, P.L1e, geo_embed(P, sm), opB, tw, r);
+  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs);
   const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
   const int64_t hstride = n / 2;  // double2 per history row
   double acc = 0.0;
   TSF_PT0();
-  for_elems<VPT>(npc, [&](int, int e) {
+  TSF_FOR_E(npc) {
     double2 g = Y[pidx(e)];
     if (j >= 1) {
       double2 h0 = cscale(H[e], I.hwe[j]);
@@ -942,126 +1150,146 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Inst &I, i
     sm.A[pidx(e)] = g;
     sm.A[pidx(e + npc)] = zero2();
     acc += cdot(g, g);
-  });
+  }
   TSF_PACC(sm, PS_RHS_HIST);
   return acc;
 }
 
 // ------------------------------------------------------------------------ one level
 // All control flow is uniform over the cluster (every CTA reduces to identical scalars).
-template <int C, int METHOD, int VPT, bool STG>
-__device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, int64_t j, const Smem &sm,
-                                            uint32_t r, VecT<VPT> &U) {
+// SHCTX: ctx lives in shared memory (single-CTA instances, where registers are scarce: two CTAs
+// per SM); otherwise ctx is this thread's register copy (clusters: one CTA per SM, and the
+// operator fields sit on the critical path of every exchange).
+template <int C, int METHOD, bool STG, bool SHCTX>
+__device__ __forceinline__ void level_solve(const DevParams &P, Ctx &ctx, int64_t j, uint32_t r, Xch &xs) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
-  const Geo ge = geo_embed(P, sm), gp = geo_prec(P, sm);
-  VecT<VPT> X, R, RH, PV, VV, S, PH, SH;
-  if constexpr (VPT == 0) {
-    const int off = int(r) * npc;
-    bind(X, I.vec, n, V_X, off); bind(R, I.vec, n, V_R, off); bind(RH, I.vec, n, V_RH, off);
-    bind(PV, I.vec, n, V_P, off); bind(VV, I.vec, n, V_V, off); bind(S, I.vec, n, V_S, off);
-    bind(PH, I.vec, n, V_PH, off); bind(SH, I.vec, n, V_SH, off);
+  if constexpr (SHCTX) {
+    ctx_ops(ctx, P, j, r);
+    __syncthreads();
   }
-  int par = 0;
+  // register copies (cluster kernels) of the context; unused when SHCTX
+  Smem lsm;
+  Inst lI;
+  Vecs lV;
+  Geo lge, lgp;
+  SpecOp lA, lB, lAT, lP, lPT;
+  if constexpr (!SHCTX) {
+    lsm = ctx.sm; lI = ctx.I; lV = ctx.V; lge = ctx.ge; lgp = ctx.gp;
+    lA = make_op(P, lI, j, OP_A, r, lsm);
+    lB = make_op(P, lI, j, OP_B, r, lsm);
+    lAT = make_op(P, lI, j, OP_AT, r, lsm);
+    lP = make_op(P, lI, j, OP_PINV, r, lsm);
+    lPT = make_op(P, lI, j, OP_PTINV, r, lsm);
+  }
+  const Smem &sm = SHCTX ? ctx.sm : lsm;
+  const Inst &I = SHCTX ? ctx.I : lI;
+  const Vecs &V = SHCTX ? ctx.V : lV;
+  const Geo &ge = SHCTX ? ctx.ge : lge, &gp = SHCTX ? ctx.gp : lgp;
+  const SpecOp &opB = SHCTX ? ctx.op[OP_B] : lB;
+  double2 *__restrict__ X = V.X, *__restrict__ R = V.R, *__restrict__ RH = V.RH, *__restrict__ PV = V.P;
+  double2 *__restrict__ VV = V.V, *__restrict__ S = V.S, *__restrict__ PH = V.PH, *__restrict__ SH = V.SH;
 #ifdef TSF_PROFILE
   const long long tlev0 = clock64();
 #endif
 
-  double g2[1] = {rhs_phase<C, VPT, STG>(P, I, j, sm, r, U)};
-  for_elems<VPT>(npc, [&](int q, int e) {
+  double g2[1] = {rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, xs)};
+  TSF_FOR_E(npc) {
     const double2 g = sm.A[pidx(e)];
-    R(q, e) = g;
-    if (METHOD == TSF_BICGSTAB) { RH(q, e) = g; PV(q, e) = g; }
-    X(q, e) = zero2();
-  });
-  csum<C, 1>(g2, sm, par);
+    R[e] = g;
+    if (METHOD == TSF_BICGSTAB) { RH[e] = g; PV[e] = g; }
+    X[e] = zero2();
+  }
+  csum<C, 1>(g2, sm, xs);
   const double rr0 = g2[0];
   const double rn0 = sqrt(rr0);
   int hs = 0, status = TSF_LEVEL_OK;
   double relres = 0.0;
-  const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
-  const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
+  const SpecOp &opA = SHCTX ? ctx.op[OP_A] : lA;
+  const SpecOp &opP = SHCTX ? ctx.op[OP_PINV] : lP;
   const double2 *Y = sm.A;      // output buffer of the last operator application
 
   if (rr0 > 0.0 && METHOD == TSF_BICGSTAB) {
     double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
     for (int it = 0;; ++it) {
       // Phase A: p = r + beta (p - omega v); phat = P^{-1} p; v = A phat; r^.v
-      for_elems<VPT>(npc, [&](int q, int e) {
-        double2 pv;
-        if (it == 0) pv = R(q, e);
-        else {
-          pv = caxpy(beta, caxpy(-omega, VV(q, e), PV(q, e)), R(q, e));
-          PV(q, e) = pv;
-        }
-        sm.A[pidx(e)] = pv;
-      });
+      if (it == 0) {
+        TSF_FOR_E(npc) { sm.A[pidx(e)] = R[e]; }
+      } else {
+        batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
+                       [&](int e, T3 &t) {
+                         const double2 pv = caxpy(beta, caxpy(-omega, t.b, t.c), t.a);
+                         PV[e] = pv;
+                         sm.A[pidx(e)] = pv;
+                       });
+      }
       __syncthreads();
-      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
-      for_elems<VPT>(npc, [&](int q, int e) {
+      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
+      TSF_FOR_E(npc) {
         const double2 ph = Y[pidx(e)];
-        PH(q, e) = ph;
+        PH[e] = ph;
         sm.A[pidx(e)] = ph;
         sm.A[pidx(e + npc)] = zero2();
-      });
+      }
       __syncthreads();
-      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
       double d[1] = {0.0};
-      for_elems<VPT>(npc, [&](int q, int e) {
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; }, [&](int e, T1 &t) {
         const double2 v = Y[pidx(e)];
-        VV(q, e) = v;
-        d[0] += cdot(RH(q, e), v);
+        VV[e] = v;
+        d[0] += cdot(t.a, v);
       });
-      csum<C, 1>(d, sm, par);
+      csum<C, 1>(d, sm, xs);
       if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       alpha = rho / d[0];
       // Phase B: s = r - alpha v; half-step exit on ||s||
       double ss[1] = {0.0};
-      for_elems<VPT>(npc, [&](int q, int e) {
-        const double2 s = caxpy(-alpha, VV(q, e), R(q, e));
-        S(q, e) = s;
+      batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = VV[e]; t.b = R[e]; }, [&](int e, T2 &t) {
+        const double2 s = caxpy(-alpha, t.a, t.b);
+        S[e] = s;
         sm.A[pidx(e)] = s;
         ss[0] += cdot(s, s);
       });
-      csum<C, 1>(ss, sm, par);
+      csum<C, 1>(ss, sm, xs);
       if (sqrt(ss[0]) < P.tol * rn0) {
-        for_elems<VPT>(npc, [&](int q, int e) { X(q, e) = caxpy(alpha, PH(q, e), X(q, e)); });
+        batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = PH[e]; t.b = X[e]; },
+                       [&](int e, T2 &t) { X[e] = caxpy(alpha, t.a, t.b); });
         hs += 1;
         relres = sqrt(ss[0]) / rn0;
         break;
       }
       //          shat = P^{-1} s; t = A shat; t.s, t.t
-      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
-      for_elems<VPT>(npc, [&](int q, int e) {
+      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
+      TSF_FOR_E(npc) {
         const double2 sh = Y[pidx(e)];
-        SH(q, e) = sh;
+        SH[e] = sh;
         sm.A[pidx(e)] = sh;
         sm.A[pidx(e + npc)] = zero2();
-      });
+      }
       __syncthreads();
-      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
       double tt[2] = {0.0, 0.0};
-      for_elems<VPT>(npc, [&](int q, int e) {
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = S[e]; }, [&](int e, T1 &ts) {
         const double2 t = Y[pidx(e)];
-        const double2 s = S(q, e);
-        tt[0] += cdot(t, s);
+        tt[0] += cdot(t, ts.a);
         tt[1] += cdot(t, t);
       });
-      csum<C, 2>(tt, sm, par);
+      csum<C, 2>(tt, sm, xs);
       if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       omega = tt[0] / tt[1];
       // Phase C: x += alpha phat + omega shat; r = s - omega t; r^.r, r.r
       double rr[2] = {0.0, 0.0};
-      for_elems<VPT>(npc, [&](int q, int e) {
-        X(q, e) = caxpy(omega, SH(q, e), caxpy(alpha, PH(q, e), X(q, e)));
-        const double2 rn = caxpy(-omega, Y[pidx(e)], S(q, e));
-        R(q, e) = rn;
-        rr[0] += cdot(RH(q, e), rn);
-        rr[1] += cdot(rn, rn);
-      });
-      csum<C, 2>(rr, sm, par);
+      batched<(TSF_BATCH > 2 ? 2 : TSF_BATCH), T5>(npc, [&](int e, T5 &t) { t.a = X[e]; t.b = SH[e]; t.c = PH[e]; t.d = S[e]; t.f = RH[e]; },
+                     [&](int e, T5 &t) {
+                       X[e] = caxpy(omega, t.b, caxpy(alpha, t.c, t.a));
+                       const double2 rn = caxpy(-omega, Y[pidx(e)], t.d);
+                       R[e] = rn;
+                       rr[0] += cdot(t.f, rn);
+                       rr[1] += cdot(rn, rn);
+                     });
+      csum<C, 2>(rr, sm, xs);
       hs += 2;
       relres = sqrt(rr[1]) / rn0;
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
@@ -1073,64 +1301,63 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
     }
   } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
     // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r, p = z.
-    const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
-    const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
+    const SpecOp &opAT = SHCTX ? ctx.op[OP_AT] : lAT;
+    const SpecOp &opPT = SHCTX ? ctx.op[OP_PTINV] : lPT;
     // z = P^{-T} (A^T r): A^T on the padded input, then P^{-T} on its first npc values
     auto ktrans = [&]() -> const double2 * {
-      const double2 *Z = apply<C, false, STG>(sm, P.L1e, ge, opAT, tw, r);
+      const double2 *Z = apply<C, STG>(sm, P.L1e, ge, opAT, tw, r, xs);
       if (!prec) return Z;
       if (Z != sm.A) {
-        for_elems<VPT>(npc, [&](int, int e) { sm.A[pidx(e)] = Z[pidx(e)]; });
+        TSF_FOR_E(npc) { sm.A[pidx(e)] = Z[pidx(e)]; }
         __syncthreads();
       }
-      return apply<C, true, STG>(sm, P.L1e, gp, opPT, tw, r);
+      return apply<C, STG>(sm, P.L1e, gp, opPT, tw, r, xs);
     };
     // A[0..npc) holds r = g and A[npc..) is zero (rhs_phase)
     __syncthreads();
     Y = ktrans();
     double gz[1] = {0.0};
-    for_elems<VPT>(npc, [&](int q, int e) {
+    TSF_FOR_E(npc) {
       const double2 z = Y[pidx(e)];
-      PV(q, e) = z;
+      PV[e] = z;
       gz[0] += cdot(z, z);
-    });
-    csum<C, 1>(gz, sm, par);
+    }
+    csum<C, 1>(gz, sm, xs);
     double gam = gz[0];
     double beta = 0.0;
     for (int it = 0;; ++it) {
       // Phase A: p = z + beta p; phat = P^{-1} p; q = A phat; ||q||^2
-      for_elems<VPT>(npc, [&](int q, int e) {
-        double2 pv;
-        if (it == 0) pv = PV(q, e);
-        else { pv = caxpy(beta, PV(q, e), Y[pidx(e)]); PV(q, e) = pv; }
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = PV[e]; }, [&](int e, T1 &t) {
+        double2 pv = t.a;
+        if (it != 0) { pv = caxpy(beta, t.a, Y[pidx(e)]); PV[e] = pv; }
         sm.A[pidx(e)] = pv;
       });
       __syncthreads();
-      Y = prec ? apply<C, true, STG>(sm, P.L1e, gp, opP, tw, r) : sm.A;
-      for_elems<VPT>(npc, [&](int q, int e) {
+      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
+      TSF_FOR_E(npc) {
         const double2 ph = Y[pidx(e)];
-        PH(q, e) = ph;
+        PH[e] = ph;
         sm.A[pidx(e)] = ph;
         sm.A[pidx(e + npc)] = zero2();
-      });
+      }
       __syncthreads();
-      Y = apply<C, false, STG>(sm, P.L1e, ge, opA, tw, r);
+      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
       double qq[1] = {0.0};
-      for_elems<VPT>(npc, [&](int, int e) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); });
-      csum<C, 1>(qq, sm, par);
+      TSF_FOR_E(npc) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+      csum<C, 1>(qq, sm, xs);
       if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       const double a = gam / qq[0];
       // Phase B: x += a phat; r -= a q; ||r||; z = P^{-T} A^T r; ||z||^2
       double rl[1] = {0.0};
-      for_elems<VPT>(npc, [&](int q, int e) {
-        X(q, e) = caxpy(a, PH(q, e), X(q, e));
-        const double2 rn = caxpy(-a, Y[pidx(e)], R(q, e));
-        R(q, e) = rn;
+      batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = X[e]; t.b = PH[e]; t.c = R[e]; }, [&](int e, T3 &t) {
+        X[e] = caxpy(a, t.b, t.a);
+        const double2 rn = caxpy(-a, Y[pidx(e)], t.c);
+        R[e] = rn;
         sm.A[pidx(e)] = rn;
         sm.A[pidx(e + npc)] = zero2();
         rl[0] += cdot(rn, rn);
       });
-      csum<C, 1>(rl, sm, par);
+      csum<C, 1>(rl, sm, xs);
       hs += 2;
       relres = sqrt(rl[0] / rr0);
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
@@ -1138,18 +1365,17 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
       Y = ktrans();
       double zz[1] = {0.0};
-      for_elems<VPT>(npc, [&](int, int e) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); });
-      csum<C, 1>(zz, sm, par);
+      TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+      csum<C, 1>(zz, sm, xs);
       beta = zz[0] / gam;
       gam = zz[0];
     }
   }
   // finalize (alg1 step 3 result): d^j = u^{j+1} - u^j, u^j <- u^{j+1}
   double2 *Hj = reinterpret_cast<double2 *>(I.hist + j * n) + r * npc;
-  for_elems<VPT>(npc, [&](int q, int e) {
-    const double2 x = X(q, e), u = U(q, e);
-    Hj[e] = csub(x, u);
-    U(q, e) = x;
+  batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = X[e]; t.b = V.U[e]; }, [&](int e, T2 &t) {
+    Hj[e] = csub(t.a, t.b);
+    V.U[e] = t.a;
   });
   if (r == 0 && threadIdx.x == 0) {
     I.it[j] = hs;
@@ -1166,24 +1392,28 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, i
 }
 
 // ------------------------------------------------------------------------ kernels
-template <int C, int METHOD, int VPT, bool STG>
-__global__ void __launch_bounds__(kThreads, (C == 1 && VPT == 0) ? 2 : 1)
+template <int C, int METHOD, bool STG>
+__global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
     k_solve(DevParams P, int32_t nlev, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctx ctx;
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
-  const Inst I = inst_view(P, b);
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  ctx_init(ctx, P, smem_raw, b, r);
+  const Smem &sm = ctx.sm;
+  const Inst &I = ctx.I;
+  const Vecs &V = ctx.V;
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
-  VecT<VPT> U;
   double2 *Ug = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
-  if constexpr (VPT > 0) for_elems<VPT>(npc, [&](int q, int e) { U(q, e) = Ug[e]; });
-  else U.p = Ug;
+  if (sm.vs) TSF_FOR_E(npc) { V.U[e] = Ug[e]; }
   __syncthreads();
+  xinit<C>(sm);
+  Xch xs;
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, VPT, STG>(P, I, j, sm, r, U);
-  if constexpr (VPT > 0) for_elems<VPT>(npc, [&](int q, int e) { Ug[e] = U(q, e); });
+  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG, C == 1>(P, ctx, j, r, xs);
+  if (sm.vs) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
+  csync<C>();                    // no CTA leaves while a peer may still push into it
 }
 
 __global__ void k_advance(int64_t *level, int64_t by, int64_t M);
@@ -1193,9 +1423,11 @@ template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t, int b, int64_t j,
                                                               int which, const double *in, double *out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctx ctx;
   const uint32_t r = crank<C>();
-  const Inst I = inst_view(P, b);
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  ctx_init(ctx, P, smem_raw, b, r);
+  const Smem &sm = ctx.sm;
+  const Inst &I = ctx.I;
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   const double2 *X = reinterpret_cast<const double2 *>(in) + r * npc;
@@ -1207,30 +1439,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
     if (embed) sm.A[pidx(e + npc)] = zero2();
   }
   __syncthreads();
-  const SpecOp op = make_op(P, I, j, which, r, sm);
-  const double2 *Z = embed ? apply<C, false, STG>(sm, P.L1e, geo_embed(P, sm), op, tw, r)
-                           : apply<C, true, STG>(sm, P.L1e, geo_prec(P, sm), op, tw, r);
+  xinit<C>(sm);
+  Xch xs;
+  ctx_ops(ctx, P, j, r);
+  __syncthreads();
+  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? ctx.ge : ctx.gp, ctx.op[which], tw, r, xs);
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
+  csync<C>();
 }
 
 // Debug: RHS of the current level for every instance into V_R.
 template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Ctx ctx;
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
-  const Inst I = inst_view(P, b);
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.prof);
+  ctx_init(ctx, P, smem_raw, b, r);
+  const Smem &sm = ctx.sm;
+  const Inst &I = ctx.I;
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int64_t j = *P.level;
   const int npc = P.L1p;
   __syncthreads();
   if (j >= P.M) return;
-  VecT<0> U;
-  U.p = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
-  rhs_phase<C, 0, STG>(P, I, j, sm, r, U);
+  xinit<C>(sm);
+  Xch xs;
+  ctx_ops(ctx, P, j, r);
+  __syncthreads();
+  const double2 *U = reinterpret_cast<const double2 *>(I.vec + V_U * P.n) + r * npc;
+  rhs_phase<C, STG>(P, sm, I, ctx.ge, ctx.op[OP_B], j, r, U, xs);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
   for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
+  csync<C>();
 }
 
 // ------------------------------------------------------------------------ launch API
@@ -1267,8 +1508,7 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// Staged exchange (STG) exists for C > 1 only; register-resident vectors (VPT > 0) are
-// planned only together with the staged exchange or C == 1.
+// Staged exchange (STG) exists for C > 1 only.
 #define TSF_STG_OF(CC, pl) ((CC) > 1 && (pl).staged)
 #define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
   template <>                                                                                   \
@@ -1277,15 +1517,11 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
     const int32_t z = 0;                                                                        \
     constexpr bool S1 = (CC) > 1;                                                               \
     if (pl.method == TSF_BICGSTAB) {                                                            \
-      if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 1, S1>, pl, g, st, dp, nlev, z); \
-      if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 2, S1>, pl, g, st, dp, nlev, z); \
-      if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0, S1>, pl, g, st, dp, nlev, z); \
-      return launch_cluster(k_solve<CC, TSF_BICGSTAB, 0, false>, pl, g, st, dp, nlev, z);       \
+      if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1>, pl, g, st, dp, nlev, z); \
+      return launch_cluster(k_solve<CC, TSF_BICGSTAB, false>, pl, g, st, dp, nlev, z);          \
     }                                                                                           \
-    if (pl.vpt == 1) return launch_cluster(k_solve<CC, TSF_CGNR, 1, S1>, pl, g, st, dp, nlev, z); \
-    if (pl.vpt == 2) return launch_cluster(k_solve<CC, TSF_CGNR, 2, S1>, pl, g, st, dp, nlev, z); \
-    if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_CGNR, 0, S1>, pl, g, st, dp, nlev, z); \
-    return launch_cluster(k_solve<CC, TSF_CGNR, 0, false>, pl, g, st, dp, nlev, z);             \
+    if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_CGNR, S1>, pl, g, st, dp, nlev, z); \
+    return launch_cluster(k_solve<CC, TSF_CGNR, false>, pl, g, st, dp, nlev, z);                \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \

@@ -141,18 +141,21 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.L1p = int32_t(n / (2 * C));
   P.npe = P.L1e / (2 * C);
   P.npp = P.L1p / (2 * C);
-  // Krylov vectors in registers when a CTA's chunk is at most 2 complex values per thread
-  const int64_t npc = n / (2 * C);
-  P.vpt = npc <= kThreads ? 1 : (npc <= 2 * kThreads ? 2 : 0);
-  if (const char *ev = std::getenv("TSF_VPT")) P.vpt = std::atoi(ev);
-  if (C > 1 && n / C > 4096) P.vpt = 0;  // register exchange path keeps vectors in HBM
   // staged cross-CTA exchange when three local buffers fit (L1e <= 4096); constant tables
   // resident in SMEM when they fit too (L1e <= 1024)
   P.staged = (C > 1 && P.L1e <= 4096) ? 1 : 0;
   if (const char *es = std::getenv("TSF_STAGED")) P.staged = (C > 1) ? std::atoi(es) : 0;
   P.resident = (P.staged && P.L1e <= 1024) ? 1 : 0;
   if (const char *er = std::getenv("TSF_RESIDENT")) P.resident = P.staged ? std::atoi(er) : 0;
-  P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident);
+  // Krylov vectors in SMEM when they fit next to the transform buffers (one CTA per SM for
+  // clusters; single-CTA instances keep two CTAs per SM)
+  {
+    const int64_t with = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, 1);
+    P.vsmem = (with <= (C > 1 ? kMaxSmem : kMaxSmem / 2 - 1024)) ? 1 : 0;
+    if (const char *ev = std::getenv("TSF_VSMEM")) P.vsmem = (with <= kMaxSmem) ? std::atoi(ev) : 0;
+  }
+  P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem);
+  if (const char *ef = std::getenv("TSF_FUSE_MIN")) P.fuse_min = std::atoi(ef);
 
   // shared tables
   size_t o = 0;
@@ -284,7 +287,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.n = pl.n; d.M = pl.M; d.B = pl.B; d.C = pl.C; d.K = pl.K; d.src_kind = pl.src_kind;
   d.method = pl.method; d.precond = pl.precond; d.maxit = pl.maxit;
   d.L1e = pl.L1e; d.L1p = pl.L1p; d.npe = pl.npe; d.npp = pl.npp;
-  d.staged = pl.staged; d.resident = pl.resident;
+  d.staged = pl.staged; d.resident = pl.resident; d.vsmem = pl.vsmem; d.fuse_min = pl.fuse_min;
   d.tol = pl.tol;
   d.scale_e = 1.0 / (4.0 * double(pl.n));
   d.scale_p = 1.0 / (4.0 * double(pl.n / 2));

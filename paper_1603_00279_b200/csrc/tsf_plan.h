@@ -16,6 +16,8 @@ namespace tsf {
 constexpr int kThreads = 256;          // threads per CTA
 constexpr int kMaxLocal = 8192;        // max complex elements of the local FFT (128 KiB)
 constexpr int kNumVec = 11;            // u, Krylov work vectors, phi copy
+constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^)
+constexpr int64_t kMaxSmem = 232448;   // opt-in dynamic shared memory per CTA (227 KiB)
 constexpr size_t kAlign = 256;
 
 // Vector slots inside the per-instance vector block (each n doubles).
@@ -27,6 +29,8 @@ struct DevParams {
   int32_t B, C, K, src_kind, method, precond, maxit;
   int32_t L1e, L1p, npe, npp;      // local FFT lengths and column-pair tasks per CTA
   int32_t staged, resident;        // exchange / SMEM-table modes (see Plan)
+  int32_t vsmem;                   // Krylov vectors in SMEM (else in the instance's HBM block)
+  int32_t fuse_min;                // local FFT length from which radix-16 passes are used
   double tol;
   double scale_e, scale_p;         // 1/(4L) folding of the real-FFT split and 1/L
   double qscale_p;                 // Lambda_Q scale of the preconditioner: 1 or (n-1)/n
@@ -51,9 +55,10 @@ struct Plan {
   int32_t method = 0, precond = 0, maxit = 0;
   double tol = 0;
   int32_t L1e = 0, L1p = 0, npe = 0, npp = 0;
-  int32_t vpt = 0;      // Krylov vectors in registers: complex values per thread (0 = global)
+  int32_t vsmem = 0;    // Krylov vectors of a CTA's chunk resident in SMEM (else HBM)
   int32_t staged = 0;   // cross-CTA step staged through SMEM buffers B (staging) and O (output)
   int32_t resident = 0; // per-instance constant tables cached in SMEM (small local length)
+  int32_t fuse_min = 16 * kThreads;
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
@@ -119,14 +124,15 @@ DevParams dev_params(const Plan &pl, char *ws);
 // Shared-memory carve-up of the solve kernel (must match smem_view in tsf_kernels.cuh):
 // A [L1e], B [L1e] and O [L1e] if staged, twiddles (direct [L1e] if resident, else two-level
 // [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], base spectra [L1e + L1p],
-// pair twiddles [L1e + L1p] (double2) and sine tables [L1e + L1p] (double); 48 doubles of
-// reduction scratch.
-TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident) {
-  const int64_t L1pad = L1e + L1e / 16;           // padded transform buffers (pidx)
-  int64_t c2 = staged ? (2 * L1pad + L1e) : L1pad;
+// pair twiddles [L1e + L1p] (double2), Krylov vectors [kSmemVec x L1p] (double2) if vsmem, and
+// sine tables [L1e + L1p] (double); 48 doubles of reduction scratch, 128 doubles of pushed CTA
+// partials and 4 mbarriers.
+TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem) {
+  int64_t c2 = staged ? 3 * L1e : L1e;            // transform buffers A (+ B, O)
   if (resident) c2 += L1e + 3 * (L1e + L1p);
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
-  int64_t d = 48 + (resident ? (L1e + L1p) : 0);
+  if (vsmem) c2 += kSmemVec * L1p;
+  int64_t d = 48 + 128 + 4 + (resident ? (L1e + L1p) : 0);   // reductions, push buffers, mbarriers
   return 16 * c2 + 8 * d + 64;
 }
 

@@ -206,8 +206,8 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   s.prof = prof;
   s.fuse_min = fuse_min;
   double2 *c = reinterpret_cast<double2 *>(raw);
-  s.A = c; c += L1e;
-  if (staged) { s.B = c; c += L1e; s.O = c; c += L1e; }
+  s.A = c; c += L1e + kPadBuf * (L1e / 16);
+  if (staged) { s.B = c; c += L1e; s.O = c; c += L1e + kPadBuf * (L1e / 16); }
   if (resident) {
     s.twd = c; c += L1e;
     s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
@@ -396,7 +396,11 @@ __device__ __forceinline__ void bfly4(double2 &a0, double2 &a1, double2 &a2, dou
 // makes every radix-4 / radix-2 stage, every fused radix-16 pass and the linear loops free of
 // shared-memory bank conflicts, and keeps the digit-reversed pair reads <= ~2.3-way
 // (tools/smem_conflicts.py, L1 = 2^8..2^13).
+#ifdef TSF_PAD
+__device__ __forceinline__ int pidx(int p) { return p + (p >> 4); }
+#else
 __device__ __forceinline__ int pidx(int p) { return p ^ (((p >> 2) ^ (p >> 5) ^ (p >> 9)) & 7); }
+#endif
 
 // one stage: m = 2^lm, twiddle W_m^{kq} = W_{L1e}^{kq (L1e/m)}
 template <bool INV, int RADIX>
@@ -623,14 +627,6 @@ struct SpecOp {
     const double im = pmq * b.y + c2 * s;
     return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
   }
-  // lam_idx for tables known to be in global memory (read-only path, freely reordered)
-  __device__ __forceinline__ double2 lam_idx_g(int idx, int bin) const {
-    const double2 b = __ldg(lam + idx);
-    const double s = __ldg(sq + idx);
-    const double re = ppq * b.x + ((bin & 1) ? -qcorr : qcorr);
-    const double im = pmq * b.y + c2 * s;
-    return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
-  }
   // effective multiplier (lambda or 1/lambda) of bin (k2, ab, i)
   __device__ __forceinline__ double2 get(int k2, int ab, int i, int bin) const {
     return eff(lam_idx(((rC + k2) * 2 + ab) * np + i, bin));
@@ -678,27 +674,24 @@ struct Geo {
   const double2 *ctw;         // resident column twiddles W_L^{q k1(col)} [q ncol + col]
 };
 
-// C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).  The spectra and
-// twiddles are global (read-only path, so loads of later pairs overlap earlier arithmetic).
+// C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).  Slots come from
+// the exported slot table (L1-resident; measured faster here than the closed-form dslot).
 __device__ __forceinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
                                              const double2 *__restrict__ tw) {
-  if (threadIdx.x == 0) {
-    const int sa = pidx(dslot(0, g.l1)), sb = pidx(dslot(g.L1 / 2, g.l1));
-    double2 a = A[sa], b = A[sb];
-    pair_self(a, op.eff(op.lam_idx_g(0, 0)), op.nyquist(g.L), __ldg(tw), op.scale);
-    const double2 lm = op.eff(op.lam_idx_g(g.np, g.L / 2));
-    pair_self(b, lm, lm, __ldg(tw + (g.L / 2) * g.tw2L), op.scale);
-    A[sa] = a; A[sb] = b;
-  }
-#pragma unroll 4
-  for (int i = threadIdx.x + 1; i < g.np; i += kThreads) {
-    const double2 la = op.eff(op.lam_idx_g(i, i));
-    const double2 lb = op.eff(op.lam_idx_g(g.np + i, g.L - i));
-    const double2 w = __ldg(tw + i * g.tw2L);
-    const int sa = pidx(dslot(i, g.l1)), sb = pidx(dslot(g.L1 - i, g.l1));
-    double2 a = A[sa], b = A[sb];
-    pair_apply(a, b, la, lb, w, op.scale);
-    A[sa] = a; A[sb] = b;
+  for (int i = threadIdx.x; i < g.np; i += kThreads) {
+    if (i == 0) {
+      const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
+      double2 a = A[sa], b = A[sb];
+      pair_self(a, op.get(0, 0, 0, 0), op.nyquist(g.L), tw[0], op.scale);
+      const double2 lm = op.get(0, 1, 0, g.L / 2);
+      pair_self(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
+      A[sa] = a; A[sb] = b;
+    } else {
+      const int sa = pidx(g.slot[i]), sb = pidx(g.slot[g.L1 - i]);
+      double2 a = A[sa], b = A[sb];
+      pair_apply(a, b, op.get(0, 0, i, i), op.get(0, 1, i, g.L - i), tw[i * g.tw2L], op.scale);
+      A[sa] = a; A[sb] = b;
+    }
   }
 }
 
@@ -1049,16 +1042,13 @@ __device__ __forceinline__ Vecs vec_view(const DevParams &P, const Inst &I, cons
   return v;
 }
 
-// Per-CTA context in shared memory: carve-up, instance view, vector pointers, transform
-// geometries and the level's five operators.  Kept in SMEM rather than registers: as register
-// values these ~160 words of bookkeeping stay live across a whole Krylov iteration and force
-// spills; from SMEM they are reloaded (LDS, broadcast) after every barrier instead.
+// Per-CTA context (carve-up, instance view, vector pointers, transform geometries), built once
+// by thread 0 in shared memory and copied by every thread.
 struct Ctx {
   Smem sm;
   Inst I;
   Vecs V;
   Geo ge, gp;
-  SpecOp op[5];
 };
 
 __device__ __forceinline__ void ctx_init(Ctx &ctx, const DevParams &P, unsigned char *raw, int b, uint32_t r) {
@@ -1070,10 +1060,6 @@ __device__ __forceinline__ void ctx_init(Ctx &ctx, const DevParams &P, unsigned 
     ctx.gp = geo_prec(P, ctx.sm);
   }
   __syncthreads();
-}
-// level-j operators A, B, A^T, P^{-1}, P^{-T} into ctx.op (caller synchronizes)
-__device__ __forceinline__ void ctx_ops(Ctx &ctx, const DevParams &P, int64_t j, uint32_t r) {
-  if (threadIdx.x < 5) ctx.op[threadIdx.x] = make_op(P, ctx.I, j, int(threadIdx.x), r, ctx.sm);
 }
 
 #define TSF_FOR_E(npc) for (int e = threadIdx.x; e < (npc); e += kThreads)
@@ -1157,38 +1143,22 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
 
 // ------------------------------------------------------------------------ one level
 // All control flow is uniform over the cluster (every CTA reduces to identical scalars).
-// SHCTX: ctx lives in shared memory (single-CTA instances, where registers are scarce: two CTAs
-// per SM); otherwise ctx is this thread's register copy (clusters: one CTA per SM, and the
-// operator fields sit on the critical path of every exchange).
-template <int C, int METHOD, bool STG, bool SHCTX>
-__device__ __forceinline__ void level_solve(const DevParams &P, Ctx &ctx, int64_t j, uint32_t r, Xch &xs) {
+// The context is copied into registers for the level (fields of the operators and the
+// carve-up sit on the critical path of every transform; an SMEM-resident context was measured
+// slower at C3 and C4).
+template <int C, int METHOD, bool STG>
+__device__ __forceinline__ void level_solve(const DevParams &P, const Ctx &ctx, int64_t j, uint32_t r, Xch &xs) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
-  if constexpr (SHCTX) {
-    ctx_ops(ctx, P, j, r);
-    __syncthreads();
-  }
-  // register copies (cluster kernels) of the context; unused when SHCTX
-  Smem lsm;
-  Inst lI;
-  Vecs lV;
-  Geo lge, lgp;
-  SpecOp lA, lB, lAT, lP, lPT;
-  if constexpr (!SHCTX) {
-    lsm = ctx.sm; lI = ctx.I; lV = ctx.V; lge = ctx.ge; lgp = ctx.gp;
-    lA = make_op(P, lI, j, OP_A, r, lsm);
-    lB = make_op(P, lI, j, OP_B, r, lsm);
-    lAT = make_op(P, lI, j, OP_AT, r, lsm);
-    lP = make_op(P, lI, j, OP_PINV, r, lsm);
-    lPT = make_op(P, lI, j, OP_PTINV, r, lsm);
-  }
-  const Smem &sm = SHCTX ? ctx.sm : lsm;
-  const Inst &I = SHCTX ? ctx.I : lI;
-  const Vecs &V = SHCTX ? ctx.V : lV;
-  const Geo &ge = SHCTX ? ctx.ge : lge, &gp = SHCTX ? ctx.gp : lgp;
-  const SpecOp &opB = SHCTX ? ctx.op[OP_B] : lB;
+  const Smem sm = ctx.sm;
+  const Inst I = ctx.I;
+  const Vecs V = ctx.V;
+  const Geo ge = ctx.ge, gp = ctx.gp;
+  const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
+  const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
+  const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
   double2 *__restrict__ X = V.X, *__restrict__ R = V.R, *__restrict__ RH = V.RH, *__restrict__ PV = V.P;
   double2 *__restrict__ VV = V.V, *__restrict__ S = V.S, *__restrict__ PH = V.PH, *__restrict__ SH = V.SH;
 #ifdef TSF_PROFILE
@@ -1207,8 +1177,6 @@ __device__ __forceinline__ void level_solve(const DevParams &P, Ctx &ctx, int64_
   const double rn0 = sqrt(rr0);
   int hs = 0, status = TSF_LEVEL_OK;
   double relres = 0.0;
-  const SpecOp &opA = SHCTX ? ctx.op[OP_A] : lA;
-  const SpecOp &opP = SHCTX ? ctx.op[OP_PINV] : lP;
   const double2 *Y = sm.A;      // output buffer of the last operator application
 
   if (rr0 > 0.0 && METHOD == TSF_BICGSTAB) {
@@ -1301,8 +1269,8 @@ __device__ __forceinline__ void level_solve(const DevParams &P, Ctx &ctx, int64_
     }
   } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
     // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r, p = z.
-    const SpecOp &opAT = SHCTX ? ctx.op[OP_AT] : lAT;
-    const SpecOp &opPT = SHCTX ? ctx.op[OP_PTINV] : lPT;
+    const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
+    const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
     // z = P^{-T} (A^T r): A^T on the padded input, then P^{-T} on its first npc values
     auto ktrans = [&]() -> const double2 * {
       const double2 *Z = apply<C, STG>(sm, P.L1e, ge, opAT, tw, r, xs);
@@ -1411,7 +1379,7 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   xinit<C>(sm);
   Xch xs;
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG, C == 1>(P, ctx, j, r, xs);
+  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, ctx, j, r, xs);
   if (sm.vs) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
   csync<C>();                    // no CTA leaves while a peer may still push into it
 }
@@ -1441,9 +1409,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
   __syncthreads();
   xinit<C>(sm);
   Xch xs;
-  ctx_ops(ctx, P, j, r);
-  __syncthreads();
-  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? ctx.ge : ctx.gp, ctx.op[which], tw, r, xs);
+  const SpecOp op = make_op(P, I, j, which, r, sm);
+  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? ctx.ge : ctx.gp, op, tw, r, xs);
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
   csync<C>();
 }
@@ -1465,10 +1432,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
   if (j >= P.M) return;
   xinit<C>(sm);
   Xch xs;
-  ctx_ops(ctx, P, j, r);
-  __syncthreads();
+  const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const double2 *U = reinterpret_cast<const double2 *>(I.vec + V_U * P.n) + r * npc;
-  rhs_phase<C, STG>(P, sm, I, ctx.ge, ctx.op[OP_B], j, r, U, xs);
+  rhs_phase<C, STG>(P, sm, I, ctx.ge, opB, j, r, U, xs);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
   for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
   csync<C>();

@@ -19,6 +19,11 @@ constexpr int kNumVec = 11;            // u, Krylov work vectors, phi copy
 constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^)
 constexpr int64_t kMaxSmem = 232448;   // opt-in dynamic shared memory per CTA (227 KiB)
 constexpr size_t kAlign = 256;
+#ifdef TSF_PAD
+constexpr int kPadBuf = 1;             // padded transform buffers (one pad per 16 elements)
+#else
+constexpr int kPadBuf = 0;             // XOR-swizzled transform buffers need no padding
+#endif
 
 // Vector slots inside the per-instance vector block (each n doubles).
 enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_PHI };
@@ -128,7 +133,7 @@ DevParams dev_params(const Plan &pl, char *ws);
 // sine tables [L1e + L1p] (double); 48 doubles of reduction scratch, 128 doubles of pushed CTA
 // partials and 4 mbarriers.
 TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem) {
-  int64_t c2 = staged ? 3 * L1e : L1e;            // transform buffers A (+ B, O)
+  int64_t c2 = (staged ? 3 * L1e : L1e) + (staged ? 2 : 1) * kPadBuf * (L1e / 16);   // A (+ B, O)
   if (resident) c2 += L1e + 3 * (L1e + L1p);
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;

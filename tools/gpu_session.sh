@@ -27,3 +27,8 @@ echo "ncu full rc=$?" >> $O/ncu_full.log
 ncu -i $O/c3_full.ncu-rep --page raw --csv > $O/c3_full_raw.csv 2>/dev/null
 ncu -i $O/c3_full.ncu-rep --page source --csv > $O/c3_full_source.csv 2>/dev/null
 ls -la $O
+for c in C2 C4 C5; do
+  timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-e2e > $O/bench_$c.json 2> $O/bench_$c.err
+done
+python tools/ncu_keys.py $O/c3_full_raw.csv > $O/c3_full_keys.txt 2>&1
+python tools/ncu_summary.py launches $O/launches.csv > $O/launches_summary.txt 2>&1

@@ -599,6 +599,18 @@ __device__ __forceinline__ void fft_reg(double2 (&x)[N]) {
 // lambda(bin) = eta + mu * [ (p+q) Re L_W + q corr (-1)^bin + i ((p-q) Im L_W + c2 s(bin)) ]
 // for L_W the base spectrum of W (embedding, Strang or T. Chan), s the sine table of Lambda_Q,
 // optionally conjugated (A^T, P^T).  Multiply (A, B, A^T) or divide (P^{-1}, P^{-T}).
+// Explicit shared-memory loads for pointers the compiler cannot prove to be shared.
+__device__ __forceinline__ double2 lds2(const double2 *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ double lds1(const double *p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
 struct SpecOp {
   const double2 *lam;   // task-order base spectrum of this instance (SMEM slice if resident)
   const double *sq;     // task-order sine table
@@ -618,11 +630,11 @@ struct SpecOp {
   // W_{2L}^{bin} of bin (k2, ab, i): resident table or the global twiddle table
   __device__ __forceinline__ double2 wtw(int k2, int ab, int i, int bin, const double2 *tw,
                                          int tw2L) const {
-    return pw ? pw[((rC + k2) * 2 + ab) * np + i] : tw[bin * tw2L];
+    return pw ? lds2(pw + ((rC + k2) * 2 + ab) * np + i) : tw[bin * tw2L];
   }
   __device__ __forceinline__ double2 lam_idx(int idx, int bin) const {
-    const double2 b = lam[idx];
-    const double s = sq[idx];
+    const double2 b = pw ? lds2(lam + idx) : lam[idx];   // resident tables: explicit LDS
+    const double s = pw ? lds1(sq + idx) : sq[idx];
     const double re = ppq * b.x + ((bin & 1) ? -qcorr : qcorr);
     const double im = pmq * b.y + c2 * s;
     return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
@@ -1027,11 +1039,14 @@ struct Vecs {
   double2 *U, *X, *R, *RH, *P, *V, *S, *PH, *SH;
 };
 
+// VS (compile time) = vectors in SMEM, so every vector access compiles to LDS/STS or LDG/STG
+// rather than generic loads.
+template <bool VS>
 __device__ __forceinline__ Vecs vec_view(const DevParams &P, const Inst &I, const Smem &sm, uint32_t r) {
   Vecs v;
   const int npc = P.L1p;
   auto g = [&](int slot) { return reinterpret_cast<double2 *>(I.vec + slot * P.n) + r * npc; };
-  if (sm.vs) {
+  if constexpr (VS) {
     double2 *b = sm.vs;
     v.U = b; v.X = b + npc; v.R = b + 2 * npc; v.RH = b + 3 * npc; v.P = b + 4 * npc;
     v.V = b + 5 * npc; v.S = b + 6 * npc; v.PH = b + 7 * npc; v.SH = b + 8 * npc;
@@ -1040,26 +1055,6 @@ __device__ __forceinline__ Vecs vec_view(const DevParams &P, const Inst &I, cons
     v.V = g(V_V); v.S = g(V_S); v.PH = g(V_PH); v.SH = g(V_SH);
   }
   return v;
-}
-
-// Per-CTA context (carve-up, instance view, vector pointers, transform geometries), built once
-// by thread 0 in shared memory and copied by every thread.
-struct Ctx {
-  Smem sm;
-  Inst I;
-  Vecs V;
-  Geo ge, gp;
-};
-
-__device__ __forceinline__ void ctx_init(Ctx &ctx, const DevParams &P, unsigned char *raw, int b, uint32_t r) {
-  if (threadIdx.x == 0) {
-    ctx.I = inst_view(P, b);
-    ctx.sm = smem_view(raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
-    ctx.V = vec_view(P, ctx.I, ctx.sm, r);
-    ctx.ge = geo_embed(P, ctx.sm);
-    ctx.gp = geo_prec(P, ctx.sm);
-  }
-  __syncthreads();
 }
 
 #define TSF_FOR_E(npc) for (int e = threadIdx.x; e < (npc); e += kThreads)
@@ -1143,19 +1138,17 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
 
 // ------------------------------------------------------------------------ one level
 // All control flow is uniform over the cluster (every CTA reduces to identical scalars).
-// The context is copied into registers for the level (fields of the operators and the
-// carve-up sit on the critical path of every transform; an SMEM-resident context was measured
-// slower at C3 and C4).
+// Views (carve-up, instance, vectors) are computed by every thread from the kernel's own
+// pointers, so the compiler keeps SMEM accesses as LDS/STS (a view copied through shared memory
+// turned them into generic LD/ST and was measured slower).
 template <int C, int METHOD, bool STG>
-__device__ __forceinline__ void level_solve(const DevParams &P, const Ctx &ctx, int64_t j, uint32_t r, Xch &xs) {
+__device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
+                                            int64_t j, uint32_t r, Xch &xs) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
-  const Smem sm = ctx.sm;
-  const Inst I = ctx.I;
-  const Vecs V = ctx.V;
-  const Geo ge = ctx.ge, gp = ctx.gp;
+  const Geo ge = geo_embed(P, sm), gp = geo_prec(P, sm);
   const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
   const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
@@ -1360,27 +1353,25 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Ctx &ctx, 
 }
 
 // ------------------------------------------------------------------------ kernels
-template <int C, int METHOD, bool STG>
+template <int C, int METHOD, bool STG, bool VS>
 __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
     k_solve(DevParams P, int32_t nlev, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Ctx ctx;
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
-  ctx_init(ctx, P, smem_raw, b, r);
-  const Smem &sm = ctx.sm;
-  const Inst &I = ctx.I;
-  const Vecs &V = ctx.V;
+  const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+  const Vecs V = vec_view<VS>(P, I, sm, r);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   double2 *Ug = reinterpret_cast<double2 *>(I.vec + V_U * P.n) + r * npc;
-  if (sm.vs) TSF_FOR_E(npc) { V.U[e] = Ug[e]; }
+  if constexpr (VS) TSF_FOR_E(npc) { V.U[e] = Ug[e]; }
   __syncthreads();
   xinit<C>(sm);
   Xch xs;
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, ctx, j, r, xs);
-  if (sm.vs) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
+  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs);
+  if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
   csync<C>();                    // no CTA leaves while a peer may still push into it
 }
 
@@ -1391,11 +1382,9 @@ template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t, int b, int64_t j,
                                                               int which, const double *in, double *out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Ctx ctx;
   const uint32_t r = crank<C>();
-  ctx_init(ctx, P, smem_raw, b, r);
-  const Smem &sm = ctx.sm;
-  const Inst &I = ctx.I;
+  const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   const double2 *X = reinterpret_cast<const double2 *>(in) + r * npc;
@@ -1410,7 +1399,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
   xinit<C>(sm);
   Xch xs;
   const SpecOp op = make_op(P, I, j, which, r, sm);
-  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? ctx.ge : ctx.gp, op, tw, r, xs);
+  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs);
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
   csync<C>();
 }
@@ -1419,12 +1408,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
 template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Ctx ctx;
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
-  ctx_init(ctx, P, smem_raw, b, r);
-  const Smem &sm = ctx.sm;
-  const Inst &I = ctx.I;
+  const Inst I = inst_view(P, b);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int64_t j = *P.level;
   const int npc = P.L1p;
@@ -1434,7 +1421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
   Xch xs;
   const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const double2 *U = reinterpret_cast<const double2 *>(I.vec + V_U * P.n) + r * npc;
-  rhs_phase<C, STG>(P, sm, I, ctx.ge, opB, j, r, U, xs);
+  rhs_phase<C, STG>(P, sm, I, geo_embed(P, sm), opB, j, r, U, xs);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
   for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
   csync<C>();
@@ -1482,12 +1469,17 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
     const int g = pl.B * CC;                                                                    \
     const int32_t z = 0;                                                                        \
     constexpr bool S1 = (CC) > 1;                                                               \
+    const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
     if (pl.method == TSF_BICGSTAB) {                                                            \
-      if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1>, pl, g, st, dp, nlev, z); \
-      return launch_cluster(k_solve<CC, TSF_BICGSTAB, false>, pl, g, st, dp, nlev, z);          \
+      if (stg && vs) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1, true>, pl, g, st, dp, nlev, z); \
+      if (stg) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1, false>, pl, g, st, dp, nlev, z); \
+      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, CC == 1>, pl, g, st, dp, nlev, z); \
+      return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, false>, pl, g, st, dp, nlev, z);   \
     }                                                                                           \
-    if (TSF_STG_OF(CC, pl)) return launch_cluster(k_solve<CC, TSF_CGNR, S1>, pl, g, st, dp, nlev, z); \
-    return launch_cluster(k_solve<CC, TSF_CGNR, false>, pl, g, st, dp, nlev, z);                \
+    if (stg && vs) return launch_cluster(k_solve<CC, TSF_CGNR, S1, true>, pl, g, st, dp, nlev, z); \
+    if (stg) return launch_cluster(k_solve<CC, TSF_CGNR, S1, false>, pl, g, st, dp, nlev, z);   \
+    if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_CGNR, false, CC == 1>, pl, g, st, dp, nlev, z); \
+    return launch_cluster(k_solve<CC, TSF_CGNR, false, false>, pl, g, st, dp, nlev, z);         \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \

@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP64 precond-Krylov iters/s & time levels/s at N=2^14; achieved HBM GB/s"
-KRYLOV_UNITS = {"bicgstab": 26, "cgnr": 19}      # streamed units per iteration
+KRYLOV_UNITS = {"bicgstab": 26, "cgnr": 19, "pcgs": 24}   # SURVEY 8(d)-style streamed units per iteration
 
 
 def peaks():
@@ -216,7 +216,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "cgnr"])
+    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "cgnr", "pcgs"])
     ap.add_argument("--precond", default="strang", choices=["strang", "tchan", "none"])
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")

@@ -11,7 +11,7 @@
  *                   t_{j+sigma} = (j+sigma) tau, sigma = 1 - alpha/2.
  * Per level j = 0..M-1 (alg1; eq3.3):
  *     A^{(j+sigma)} u^{j+1} = B^{(j+sigma)} u^j - kappa sum_{s<j} c_{j-s}^{(j)} (u^{s+1}-u^s) + f^{j+sigma}
- * solved by right-preconditioned BiCGSTAB or CGNR (CGLS on A P^{-1}) with a Strang
+ * solved by right-preconditioned BiCGSTAB, CGNR (CGLS on A P^{-1}) or PCGS with a Strang
  * or T. Chan circulant preconditioner, x0 = 0, stop at ||r||_2/||r_0||_2 < tol
  * (P:922-925).  A and B are applied through a 2n circulant embedding and FP64 FFTs.
  *
@@ -54,7 +54,9 @@ extern "C" {
 #define TSF_LEVEL_DIVERGED 3
 #define TSF_LEVEL_SINGULAR_PREC 4
 
-typedef enum { TSF_BICGSTAB = 0, TSF_CGNR = 1 } tsf_method;
+/* TSF_PCGS: preconditioned CGS, the paper's own Krylov method (MATLAB pcgs, P:778-779,
+ * P:917-925), right-preconditioned so the stopping test uses the unpreconditioned residual. */
+typedef enum { TSF_BICGSTAB = 0, TSF_CGNR = 1, TSF_PCGS = 2 } tsf_method;
 typedef enum { TSF_STRANG = 0, TSF_TCHAN = 1, TSF_NOPREC = 2 } tsf_precond;
 typedef enum { TSF_SRC_ZERO = 0, TSF_SRC_SEPARABLE = 1, TSF_SRC_TABLE = 2 } tsf_src_kind;
 
@@ -93,7 +95,7 @@ typedef struct {
   int32_t method;     /* tsf_method  */
   int32_t precond;    /* tsf_precond */
   double tol;         /* > 0 */
-  int32_t maxit;      /* > 0; 1000 BiCGSTAB, 5000 CGNR */
+  int32_t maxit;      /* > 0; 1000 BiCGSTAB / PCGS, 5000 CGNR */
   int32_t cluster;
 } tsf_solver;
 
@@ -175,6 +177,10 @@ int tsf_debug_weights(double beta, int64_t K, double *g, double *omega);
  * solve's own fused device path.  which: 0 = A, 1 = B, 2 = A^T, 3 = P^{-1}, 4 = P^{-T}. */
 int tsf_debug_apply(tsf_handle *h, int32_t inst, int64_t j, int32_t which, const double *x,
                     double *y);
+/* Timing hook: one kernel launch running reps (>= 2) operator applications of instance inst
+ * at level j, alternating P^{-1} and A as in a Krylov iteration, on a device buffer; *ms =
+ * CUDA-event time of the launch (after one warm-up launch).  Needs a preconditioner. */
+int tsf_debug_apply_bench(tsf_handle *h, int32_t inst, int64_t j, int32_t reps, float *ms);
 /* Per-level spectra of instance `inst` in natural bin order (interleaved complex):
  * lamA[n+1] = bins 0..n of the 2n embedding of A^{(j+sigma)};
  * lamP[n/2+1] = bins 0..n/2 of the preconditioner.  Either may be NULL.              */

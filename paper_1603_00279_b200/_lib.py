@@ -18,7 +18,7 @@ TSF_OK = 0
 TSF_W_MAXIT = 1
 ERRORS = {-1: "TSF_E_ARG", -2: "TSF_E_WORKSPACE", -3: "TSF_E_CUDA", -4: "TSF_E_SINGULAR_PREC",
           -5: "TSF_E_BREAKDOWN", -6: "TSF_E_DIVERGED", -7: "TSF_E_STATE"}
-BICGSTAB, CGNR = 0, 1
+BICGSTAB, CGNR, PCGS = 0, 1, 2
 STRANG, TCHAN, NOPREC = 0, 1, 2
 SRC_ZERO, SRC_SEPARABLE, SRC_TABLE = 0, 1, 2
 
@@ -78,6 +78,7 @@ _SIGS = {
     "tsf_debug_local_fft": (C.c_int, [C.c_int64, PD, PD, C.c_int32]),
     "tsf_debug_weights": (C.c_int, [C.c_double, C.c_int64, PD, PD]),
     "tsf_debug_apply": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, PD, PD]),
+    "tsf_debug_apply_bench": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_float)]),
     "tsf_debug_spectra": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, PD, PD]),
     "tsf_debug_rhs": (C.c_int, [C.c_void_p, C.c_int32, PD]),
     "tsf_debug_set_history": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, PD]),

@@ -259,13 +259,13 @@ cudaError_t launch_solve(const Plan &pl, const DevParams &dp, int32_t nlev, cuda
 }
 
 cudaError_t launch_dbg_apply(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
-                             const double *in, double *out, cudaStream_t st) {
+                             const double *in, double *out, cudaStream_t st, int32_t reps = 0) {
   switch (pl.C) {
-    case 1: return launch_dbg_apply_c<1>(pl, dp, b, j, which, in, out, st);
-    case 2: return launch_dbg_apply_c<2>(pl, dp, b, j, which, in, out, st);
-    case 4: return launch_dbg_apply_c<4>(pl, dp, b, j, which, in, out, st);
-    case 8: return launch_dbg_apply_c<8>(pl, dp, b, j, which, in, out, st);
-    case 16: return launch_dbg_apply_c<16>(pl, dp, b, j, which, in, out, st);
+    case 1: return launch_dbg_apply_c<1>(pl, dp, b, j, which, in, out, st, reps);
+    case 2: return launch_dbg_apply_c<2>(pl, dp, b, j, which, in, out, st, reps);
+    case 4: return launch_dbg_apply_c<4>(pl, dp, b, j, which, in, out, st, reps);
+    case 8: return launch_dbg_apply_c<8>(pl, dp, b, j, which, in, out, st, reps);
+    case 16: return launch_dbg_apply_c<16>(pl, dp, b, j, which, in, out, st, reps);
   }
   return cudaErrorInvalidValue;
 }
@@ -661,6 +661,35 @@ int tsf_debug_apply(tsf_handle *h, int32_t inst, int64_t j, int32_t which, const
   CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(po.data(), dout, size_t(n) * 8, cudaMemcpyDeviceToHost));
   unpermute_host(n, h->pl.C, po.data(), y);
+  cudaFree(din);
+  cudaFree(dout);
+  return TSF_OK;
+}
+
+int tsf_debug_apply_bench(tsf_handle *h, int32_t inst, int64_t j, int32_t reps, float *ms) {
+  if (!h || !ms || inst < 0 || inst >= h->pl.B || j < 0 || j >= h->pl.M || reps < 2 ||
+      h->pl.precond == TSF_NOPREC) {
+    set_error("bad arguments");
+    return TSF_E_ARG;
+  }
+  CK(cudaSetDevice(h->device));
+  const int64_t n = h->pl.n;
+  std::vector<double> x(static_cast<size_t>(n), 1.0);
+  double *din = nullptr, *dout = nullptr;
+  CK(cudaMalloc(&din, size_t(n) * 8));
+  CK(cudaMalloc(&dout, size_t(n) * 8));
+  CK(cudaMemcpy(din, x.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+  CK(launch_dbg_apply(h->pl, h->dp, inst, j, OP_A, din, dout, h->st, reps));   // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, h->st));
+  CK(launch_dbg_apply(h->pl, h->dp, inst, j, OP_A, din, dout, h->st, reps));
+  CK(cudaEventRecord(e1, h->st));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   cudaFree(din);
   cudaFree(dout);
   return TSF_OK;

@@ -63,6 +63,7 @@ struct Inst {
   double2 *lwe, *lwp;    // base spectra, task order (+ Nyquist at the end)
   const double *lev, *hwc, *hwe, *scal, *basis, *ftab;
   double *vec, *hist;
+  double2 *mul;          // per-level multiplier tables [n + n/2] (task order), HBM variant
   int32_t *it, *st;
   double *rr;
 };
@@ -82,6 +83,7 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.ftab = reinterpret_cast<const double *>(base + P.o_ftab);
   I.vec = reinterpret_cast<double *>(base + P.o_vec);
   I.hist = reinterpret_cast<double *>(base + P.o_hist);
+  I.mul = reinterpret_cast<double2 *>(base + P.o_mul);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
   I.st = reinterpret_cast<int32_t *>(base + P.o_st);
@@ -167,8 +169,7 @@ struct Smem {
   double2 *A, *B, *O;
   double2 *twd, *thi, *tlo;          // twd != nullptr: direct table
   double2 *ctwe, *ctwp;              // column twiddles (resident)
-  double2 *lame, *lamp, *pwe, *pwp;  // base spectra / pair twiddles (resident)
-  double *sqe, *sqp;                 // sine tables (resident)
+  double2 *mule, *mulp, *pwe, *pwp;  // per-level multipliers lambda_A, 1/lambda_P / pair twiddles (resident)
   double2 *vs;                       // Krylov vectors of this CTA's chunk (kSmemVec x L1p), or null
   double *wred, *cred;
   double *red;                       // push reductions: [2][16][4] CTA partials (double-buffered)
@@ -211,7 +212,7 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   if (resident) {
     s.twd = c; c += L1e;
     s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
-    s.lame = c; c += L1e; s.lamp = c; c += L1p;
+    s.mule = c; c += L1e; s.mulp = c; c += L1p;
     s.pwe = c; c += L1e; s.pwp = c; c += L1p;
   } else {
     s.thi = c; c += tw_hi_len(L1e);
@@ -219,7 +220,6 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   }
   if (vsmem) { s.vs = c; c += kSmemVec * L1p; }
   double *d = reinterpret_cast<double *>(c);
-  if (resident) { s.sqe = d; d += L1e; s.sqp = d; d += L1p; }
   s.wred = d;
   s.cred = d + 40;
   s.red = d + 48;
@@ -263,15 +263,11 @@ __device__ __forceinline__ void load_constants(const DevParams &P, const double2
     for (int u = threadIdx.x; u < L1e; u += kThreads) {
       const int np = P.npe;
       const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
-      sm.lame[u] = lwe[int64_t(r) * L1e + u];
-      sm.sqe[u] = P.sq_e[int64_t(r) * L1e + u];
       sm.pwe[u] = tw[task_bin(L1e, C, int(r), i, k2, ab) * (P.twN / int(2 * n))];
     }
     for (int u = threadIdx.x; u < L1p; u += kThreads) {
       const int np = P.npp;
       const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
-      if (lwp) sm.lamp[u] = lwp[int64_t(r) * L1p + u];
-      sm.sqp[u] = P.sq_p[int64_t(r) * L1p + u];
       sm.pwp[u] = tw[task_bin(L1p, C, int(r), i, k2, ab) * (P.twN / int(n))];
     }
   }
@@ -612,12 +608,15 @@ __device__ __forceinline__ double lds1(const double *p) {
 }
 
 struct SpecOp {
-  const double2 *lam;   // task-order base spectrum of this instance (SMEM slice if resident)
-  const double *sq;     // task-order sine table
-  const double2 *pw;    // resident: pair twiddles W_{2L}^{bin} in task order, else nullptr
+  const double2 *lam;   // task-order base spectrum of this instance (global)
+  const double *sq;     // task-order sine table (global)
+  const double2 *mul;   // per-level effective multipliers (task order) or nullptr: then formed
+                        // from lam/sq on the fly (the once-per-level B operator)
+  const double2 *pw;    // resident: pair twiddles W_{2L}^{bin} of this CTA's slice, else nullptr
   double2 nyq;          // base spectrum at the Nyquist bin L
   int np;               // column-pair tasks per CTA
-  int rC;               // r * C (0 for resident slices)
+  int rC;               // r * C: task-order index base of this CTA in the global tables
+  bool mul_sh;          // mul is this CTA's slice in SMEM (else the global task-order table)
   double eta, mu, ppq, pmq, c2, qcorr, scale;
   bool conj;
   bool div;             // apply 1/lambda (circulant solve) instead of lambda
@@ -630,17 +629,21 @@ struct SpecOp {
   // W_{2L}^{bin} of bin (k2, ab, i): resident table or the global twiddle table
   __device__ __forceinline__ double2 wtw(int k2, int ab, int i, int bin, const double2 *tw,
                                          int tw2L) const {
-    return pw ? lds2(pw + ((rC + k2) * 2 + ab) * np + i) : tw[bin * tw2L];
+    return pw ? lds2(pw + (k2 * 2 + ab) * np + i) : tw[bin * tw2L];
   }
   __device__ __forceinline__ double2 lam_idx(int idx, int bin) const {
-    const double2 b = pw ? lds2(lam + idx) : lam[idx];   // resident tables: explicit LDS
-    const double s = pw ? lds1(sq + idx) : sq[idx];
+    const double2 b = lam[idx];
+    const double s = sq[idx];
     const double re = ppq * b.x + ((bin & 1) ? -qcorr : qcorr);
     const double im = pmq * b.y + c2 * s;
     return make_double2(eta + mu * re, conj ? -(mu * im) : mu * im);
   }
   // effective multiplier (lambda or 1/lambda) of bin (k2, ab, i)
   __device__ __forceinline__ double2 get(int k2, int ab, int i, int bin) const {
+    if (mul) {
+      const double2 m = mul_sh ? lds2(mul + (k2 * 2 + ab) * np + i) : mul[((rC + k2) * 2 + ab) * np + i];
+      return conj ? cconj(m) : m;
+    }
     return eff(lam_idx(((rC + k2) * 2 + ab) * np + i, bin));
   }
   __device__ __forceinline__ double2 nyquist_lam(int Lbin) const {
@@ -999,14 +1002,16 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
   const double eta = lv[0], c = lv[1], p = lv[2], q = lv[3];
   const double sigma = I.par[0];
   SpecOp op;
-  const bool res = sm.lame != nullptr;
-  op.rC = res ? 0 : int(r) * P.C;
+  const bool res = sm.mule != nullptr;
+  op.rC = int(r) * P.C;
+  op.mul_sh = res;
   op.eta = eta;
   op.ppq = p + q;
   op.pmq = p - q;
   if (which <= OP_AT) {
-    op.lam = res ? sm.lame : I.lwe;
-    op.sq = res ? sm.sqe : P.sq_e;
+    op.lam = I.lwe;
+    op.sq = P.sq_e;
+    op.mul = (which == OP_B) ? nullptr : (res ? sm.mule : I.mul);
     op.pw = res ? sm.pwe : nullptr;
     op.np = P.npe; op.nyq = I.lwe[P.n];
     op.mu = (which == OP_B) ? (1.0 - sigma) : -sigma;
@@ -1016,8 +1021,9 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
     op.conj = (which == OP_AT);
     op.div = false;
   } else {
-    op.lam = res ? sm.lamp : I.lwp;
-    op.sq = res ? sm.sqp : P.sq_p;
+    op.lam = I.lwp;
+    op.sq = P.sq_p;
+    op.mul = res ? sm.mulp : I.mul + P.n;
     op.pw = res ? sm.pwp : nullptr;
     op.np = P.npp; op.nyq = I.lwp[P.n / 2];
     op.mu = -sigma;
@@ -1028,6 +1034,32 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
     op.div = true;
   }
   return op;
+}
+
+// Per-level multiplier tables (task order, this CTA's slice): lambda_A of the embedding and
+// 1/lambda_P of the preconditioner, formed once per level from the base spectra so the per-bin
+// work of every operator application is a single table read (A^T, P^{-T} conjugate it).
+// Written to SMEM (resident) or the instance's HBM table; the caller synchronizes.
+__device__ __forceinline__ void fill_mul(const DevParams &P, const Inst &I, int64_t j, uint32_t r,
+                                         const Smem &sm) {
+  const Smem none = {};
+  SpecOp a = make_op(P, I, j, OP_A, r, none), pinv = make_op(P, I, j, OP_PINV, r, none);
+  const bool res = sm.mule != nullptr;
+  const int L1e = P.L1e, L1p = P.L1p, C = P.C;
+  for (int u = threadIdx.x; u < L1e; u += kThreads) {
+    const int64_t g = int64_t(r) * L1e + u;
+    const double2 v = a.lam_idx(int(g), 0);
+    if (res) sm.mule[u] = v; else I.mul[g] = v;
+  }
+  if (P.precond == TSF_NOPREC) return;
+  const int np = P.npp;
+  for (int u = threadIdx.x; u < L1p; u += kThreads) {
+    const int64_t g = int64_t(r) * L1p + u;
+    const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+    const int bin = int(task_bin(L1p, C, int(r), i, k2, ab));
+    const double2 v = pinv.eff(pinv.lam_idx(int(g), bin));
+    if (res) sm.mulp[u] = v; else I.mul[P.n + g] = v;
+  }
 }
 
 // ------------------------------------------------------------------------ vector storage
@@ -1149,6 +1181,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
   const Geo ge = geo_embed(P, sm), gp = geo_prec(P, sm);
+  fill_mul(P, I, j, r, sm);      // visible after the first barrier of rhs_phase
   const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
   const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
@@ -1163,6 +1196,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     const double2 g = sm.A[pidx(e)];
     R[e] = g;
     if (METHOD == TSF_BICGSTAB) { RH[e] = g; PV[e] = g; }
+    if (METHOD == TSF_PCGS) RH[e] = g;
     X[e] = zero2();
   }
   csum<C, 1>(g2, sm, xs);
@@ -1258,6 +1292,81 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
       if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       beta = (rr[0] / rho) * (alpha / omega);
+      rho = rr[0];
+    }
+  } else if (rr0 > 0.0 && METHOD == TSF_PCGS) {
+    // Preconditioned CGS (the paper's PCGS; MATLAB pcgs), right-preconditioned:
+    // shadow rt = r0, u = r + beta q, p = u + beta (q + beta p), phat = P^{-1} p, vhat = A phat,
+    // alpha = rho / (rt.vhat), q = u - alpha vhat, uhat = P^{-1}(u + q), x += alpha uhat,
+    // r -= alpha A uhat.  Vector slots: u -> S, p -> PV, q -> VV, phat -> PH, uhat -> SH.
+    double rho = rr0, rho_prev = 1.0;
+    for (int it = 0;; ++it) {
+      const double beta = it == 0 ? 0.0 : rho / rho_prev;
+      if (it == 0) {
+        TSF_FOR_E(npc) {
+          const double2 rv = R[e];
+          S[e] = rv;
+          PV[e] = rv;
+          sm.A[pidx(e)] = rv;
+        }
+      } else {
+        batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
+                               [&](int e, T3 &t) {
+                                 const double2 u = caxpy(beta, t.b, t.a);
+                                 const double2 pv = caxpy(beta, caxpy(beta, t.c, t.b), u);
+                                 S[e] = u;
+                                 PV[e] = pv;
+                                 sm.A[pidx(e)] = pv;
+                               });
+      }
+      __syncthreads();
+      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
+      TSF_FOR_E(npc) {
+        const double2 ph = Y[pidx(e)];
+        PH[e] = ph;
+        sm.A[pidx(e)] = ph;
+        sm.A[pidx(e + npc)] = zero2();
+      }
+      __syncthreads();
+      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+      double sg[1] = {0.0};
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; },
+                             [&](int e, T1 &t) { sg[0] += cdot(t.a, Y[pidx(e)]); });
+      csum<C, 1>(sg, sm, xs);
+      if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+      const double alpha = rho / sg[0];
+      // q = u - alpha vhat, then P^{-1}(u + q); the apply output Y still holds vhat (when Y is
+      // A itself each thread reads its element before overwriting it)
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = S[e]; }, [&](int e, T1 &t) {
+        const double2 q = caxpy(-alpha, Y[pidx(e)], t.a);
+        VV[e] = q;
+        sm.A[pidx(e)] = cadd(t.a, q);
+      });
+      __syncthreads();
+      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
+      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = X[e]; }, [&](int e, T1 &t) {
+        const double2 uh = Y[pidx(e)];
+        X[e] = caxpy(alpha, uh, t.a);
+        sm.A[pidx(e)] = uh;
+        sm.A[pidx(e + npc)] = zero2();
+      });
+      __syncthreads();
+      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+      double rr[2] = {0.0, 0.0};
+      batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = R[e]; t.b = RH[e]; }, [&](int e, T2 &t) {
+        const double2 rn = caxpy(-alpha, Y[pidx(e)], t.a);
+        R[e] = rn;
+        rr[0] += cdot(t.b, rn);
+        rr[1] += cdot(rn, rn);
+      });
+      csum<C, 2>(rr, sm, xs);
+      hs += 2;
+      relres = sqrt(rr[1]) / rn0;
+      if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+      if (relres < P.tol) break;
+      if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
+      if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+      rho_prev = rho;
       rho = rr[0];
     }
   } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
@@ -1360,7 +1469,16 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+#ifdef TSF_PROFILE
+  // section counters accumulate in SMEM (a global read-modify-write per section would stall
+  // warp 0 by an L2 round trip and inflate every section it times); flushed at the end
+  __shared__ unsigned long long prof_s[32];
+  if (threadIdx.x < 32) prof_s[threadIdx.x] = 0;
+  __syncthreads();
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min);
+#else
   const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+#endif
   const Vecs V = vec_view<VS>(P, I, sm, r);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
@@ -1372,35 +1490,62 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   const int64_t j0 = *P.level;
   for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs);
   if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
+#ifdef TSF_PROFILE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
+#endif
   csync<C>();                    // no CTA leaves while a peer may still push into it
 }
 
 __global__ void k_advance(int64_t *level, int64_t by, int64_t M);
 
 // Debug: one operator application of instance b at level j: in/out are permuted chunks.
+// reps > 1 (timing): reps applications alternating P^{-1} and A (as in a Krylov iteration),
+// each feeding the next; out holds the last result.
 template <int C, bool STG>
-__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t, int b, int64_t j,
+__global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t reps, int b, int64_t j,
                                                               int which, const double *in, double *out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
+#ifdef TSF_PROFILE
+  __shared__ unsigned long long prof_s[32];
+  if (threadIdx.x < 32) prof_s[threadIdx.x] = 0;
+  __syncthreads();
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min);
+#else
   const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+#endif
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
   const double2 *X = reinterpret_cast<const double2 *>(in) + r * npc;
   double2 *Y = reinterpret_cast<double2 *>(out) + r * npc;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  const bool embed = which <= OP_AT;
-  for (int e = threadIdx.x; e < npc; e += kThreads) {
-    sm.A[pidx(e)] = X[e];
-    if (embed) sm.A[pidx(e + npc)] = zero2();
-  }
+  for (int e = threadIdx.x; e < npc; e += kThreads) sm.A[pidx(e)] = X[e];
   __syncthreads();
   xinit<C>(sm);
   Xch xs;
-  const SpecOp op = make_op(P, I, j, which, r, sm);
-  const double2 *Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs);
+  fill_mul(P, I, j, r, sm);
+  __syncthreads();
+  const double2 *Z = sm.A;
+  const int nrep = reps > 1 ? reps : 1;
+  for (int rep = 0; rep < nrep; ++rep) {
+    const int wh = reps > 1 ? ((rep & 1) ? OP_A : OP_PINV) : which;
+    const bool embed = wh <= OP_AT;
+    for (int e = threadIdx.x; e < npc; e += kThreads) {
+      const double2 v = Z[pidx(e)];
+      sm.A[pidx(e)] = v;
+      if (embed) sm.A[pidx(e + npc)] = zero2();
+    }
+    __syncthreads();
+    const SpecOp op = make_op(P, I, j, wh, r, sm);
+    Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs);
+  }
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
+#ifdef TSF_PROFILE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
+#endif
   csync<C>();
 }
 
@@ -1433,7 +1578,7 @@ template <int C>
 cudaError_t launch_solve_c(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st);
 template <int C>
 cudaError_t launch_dbg_apply_c(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
-                               const double *in, double *out, cudaStream_t st);
+                               const double *in, double *out, cudaStream_t st, int32_t reps);
 template <int C>
 cudaError_t launch_dbg_rhs_c(const Plan &pl, const DevParams &dp, cudaStream_t st);
 
@@ -1476,6 +1621,12 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
       if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, CC == 1>, pl, g, st, dp, nlev, z); \
       return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, false>, pl, g, st, dp, nlev, z);   \
     }                                                                                           \
+    if (pl.method == TSF_PCGS) {                                                                \
+      if (stg && vs) return launch_cluster(k_solve<CC, TSF_PCGS, S1, true>, pl, g, st, dp, nlev, z); \
+      if (stg) return launch_cluster(k_solve<CC, TSF_PCGS, S1, false>, pl, g, st, dp, nlev, z);   \
+      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_PCGS, false, CC == 1>, pl, g, st, dp, nlev, z); \
+      return launch_cluster(k_solve<CC, TSF_PCGS, false, false>, pl, g, st, dp, nlev, z);         \
+    }                                                                                           \
     if (stg && vs) return launch_cluster(k_solve<CC, TSF_CGNR, S1, true>, pl, g, st, dp, nlev, z); \
     if (stg) return launch_cluster(k_solve<CC, TSF_CGNR, S1, false>, pl, g, st, dp, nlev, z);   \
     if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_CGNR, false, CC == 1>, pl, g, st, dp, nlev, z); \
@@ -1483,10 +1634,11 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \
-                                     int which, const double *in, double *out, cudaStream_t st) { \
+                                     int which, const double *in, double *out, cudaStream_t st,  \
+                                     int32_t reps) {                                             \
     if (TSF_STG_OF(CC, pl))                                                                     \
-      return launch_cluster(k_debug_apply<CC, true>, pl, CC, st, dp, int32_t(0), b, j, which, in, out); \
-    return launch_cluster(k_debug_apply<CC, false>, pl, CC, st, dp, int32_t(0), b, j, which, in, out); \
+      return launch_cluster(k_debug_apply<CC, true>, pl, CC, st, dp, reps, b, j, which, in, out); \
+    return launch_cluster(k_debug_apply<CC, false>, pl, CC, st, dp, reps, b, j, which, in, out); \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_rhs_c<CC>(const Plan &pl, const DevParams &dp, cudaStream_t st) {      \

@@ -85,7 +85,7 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
         (p[0].src_kind == TSF_SRC_SEPARABLE && p[b].K != p[0].K))
       return fail("instance %g: all instances must share n, M, source kind and K", b);
   }
-  if (s->method != TSF_BICGSTAB && s->method != TSF_CGNR) return fail("unknown method %g", s->method);
+  if (s->method != TSF_BICGSTAB && s->method != TSF_CGNR && s->method != TSF_PCGS) return fail("unknown method %g", s->method);
   if (s->precond != TSF_STRANG && s->precond != TSF_TCHAN && s->precond != TSF_NOPREC)
     return fail("unknown preconditioner %g", s->precond);
   if (!(s->tol > 0.0)) return fail("tol=%g must be > 0", s->tol);
@@ -189,6 +189,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.o_it = q;    q = up(q + size_t(P.M) * 4);
   P.o_rr = q;    q = up(q + size_t(P.M) * 8);
   P.o_st = q;    q = up(q + size_t(P.M) * 4);
+  P.o_mul = q;   q = up(q + size_t(n + n / 2) * 16);
   P.stride = q;
   P.total = P.off_inst + P.stride * size_t(B);
   *pl = P;
@@ -306,7 +307,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.o_par = pl.o_par; d.o_omega = pl.o_omega; d.o_lwe = pl.o_lwe; d.o_lwp = pl.o_lwp;
   d.o_lev = pl.o_lev; d.o_hwc = pl.o_hwc; d.o_hwe = pl.o_hwe; d.o_scal = pl.o_scal;
   d.o_basis = pl.o_basis; d.o_ftab = pl.o_ftab; d.o_vec = pl.o_vec; d.o_hist = pl.o_hist;
-  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st;
+  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul;
   return d;
 }
 

@@ -51,7 +51,7 @@ struct DevParams {
   char *inst;                      // base of instance 0
   int64_t stride;                  // bytes between instances
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul;
 };
 
 struct Plan {
@@ -71,7 +71,7 @@ struct Plan {
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul;
 };
 
 // Per-instance host tables (all doubles).
@@ -128,16 +128,15 @@ DevParams dev_params(const Plan &pl, char *ws);
 
 // Shared-memory carve-up of the solve kernel (must match smem_view in tsf_kernels.cuh):
 // A [L1e], B [L1e] and O [L1e] if staged, twiddles (direct [L1e] if resident, else two-level
-// [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], base spectra [L1e + L1p],
-// pair twiddles [L1e + L1p] (double2), Krylov vectors [kSmemVec x L1p] (double2) if vsmem, and
-// sine tables [L1e + L1p] (double); 48 doubles of reduction scratch, 128 doubles of pushed CTA
-// partials and 4 mbarriers.
+// [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], per-level multipliers
+// [L1e + L1p], pair twiddles [L1e + L1p] (double2), Krylov vectors [kSmemVec x L1p] (double2) if
+// vsmem; 48 doubles of reduction scratch, 128 doubles of pushed CTA partials and 4 mbarriers.
 TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem) {
   int64_t c2 = (staged ? 3 * L1e : L1e) + (staged ? 2 : 1) * kPadBuf * (L1e / 16);   // A (+ B, O)
-  if (resident) c2 += L1e + 3 * (L1e + L1p);
+  if (resident) c2 += L1e + 3 * (L1e + L1p);      // twiddles, column twiddles, multipliers, pair twiddles
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;
-  int64_t d = 48 + 128 + 4 + (resident ? (L1e + L1p) : 0);   // reductions, push buffers, mbarriers
+  int64_t d = 48 + 128 + 4;                        // reductions, push buffers, mbarriers
   return 16 * c2 + 8 * d + 64;
 }
 

@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib as L
 from .inputs import Instance, manufactured_basis, manufactured_scal
 
-METHODS = {"bicgstab": L.BICGSTAB, "cgnr": L.CGNR}
+METHODS = {"bicgstab": L.BICGSTAB, "cgnr": L.CGNR, "pcgs": L.PCGS}
 PRECONDS = {"strang": L.STRANG, "tchan": L.TCHAN, "none": L.NOPREC}
 
 
@@ -76,7 +76,7 @@ def make_solver_struct(method="bicgstab", precond="strang", tol=1e-12, maxit=Non
     s.method = METHODS[method]
     s.precond = PRECONDS[precond]
     s.tol = tol
-    s.maxit = maxit if maxit is not None else (1000 if method == "bicgstab" else 5000)
+    s.maxit = maxit if maxit is not None else (5000 if method == "cgnr" else 1000)
     s.cluster = cluster
     return s
 
@@ -177,6 +177,12 @@ class Solver:
         y = np.zeros(self.n)
         L.check(self.lib.tsf_debug_apply(self.h, inst, j, which, _pd(x), _pd(y)), "tsf_debug_apply")
         return y
+
+    def debug_apply_bench(self, inst: int = 0, j: int = 0, reps: int = 200) -> float:
+        """Milliseconds of one launch of `reps` alternating P^{-1} / A applications."""
+        ms = C.c_float(0.0)
+        L.check(self.lib.tsf_debug_apply_bench(self.h, inst, j, reps, C.byref(ms)), "tsf_debug_apply_bench")
+        return ms.value
 
     def debug_spectra(self, inst: int, j: int):
         la = np.zeros(2 * (self.n + 1))

@@ -399,6 +399,17 @@ __device__ __forceinline__ int pidx(int p) { return p ^ (((p >> 2) ^ (p >> 5) ^ 
 #endif
 
 // one stage: m = 2^lm, twiddle W_m^{kq} = W_{L1e}^{kq (L1e/m)}
+// Twiddles W^e, W^{2e}, W^{3e} of a radix-4 butterfly from ONE table read: the local FFTs are
+// bound by shared-memory bandwidth (16 B per complex per access, 128 B/clk/SM), and three table
+// reads per butterfly were 27% of it; the two extra complex products are free on the idle FP64
+// pipe (measured: 1024-point fwd+inv 7.5k -> 4.4k cycles, tools/fft_ubench.cu).  W^0 = 1 exactly,
+// so no k == 0 branch is needed.
+__device__ __forceinline__ void tw3(const Smem &sm, int e, double2 &w1, double2 &w2, double2 &w3) {
+  w1 = twid(sm, e);
+  w2 = cmul(w1, w1);
+  w3 = cmul(w2, w1);
+}
+
 template <bool INV, int RADIX>
 __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem &sm, int L1e) {
   const int lmp = lm - (RADIX == 4 ? 2 : 1);
@@ -411,17 +422,14 @@ __device__ __forceinline__ void fft_stage(double2 *A, int L1, int lm, const Smem
     if constexpr (RADIX == 4) {
       const int p0 = pidx(base), p1 = pidx(base + mprev), p2 = pidx(base + 2 * mprev), p3 = pidx(base + 3 * mprev);
       double2 a0 = A[p0], a1 = A[p1], a2 = A[p2], a3 = A[p3];
-      if (k != 0) {
-        const double2 w1 = twid(sm, k * tstep), w2 = twid(sm, 2 * k * tstep), w3 = twid(sm, 3 * k * tstep);
-        if (INV) {
-          a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
-          bfly4<true>(a0, a1, a2, a3);
-        } else {
-          bfly4<false>(a0, a1, a2, a3);
-          a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
-        }
+      double2 w1, w2, w3;
+      tw3(sm, k * tstep, w1, w2, w3);
+      if (INV) {
+        a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
+        bfly4<true>(a0, a1, a2, a3);
       } else {
-        bfly4<INV>(a0, a1, a2, a3);
+        bfly4<false>(a0, a1, a2, a3);
+        a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
       }
       A[p0] = a0; A[p1] = a1; A[p2] = a2; A[p3] = a3;
     } else {
@@ -460,44 +468,38 @@ __device__ __forceinline__ void fft_pass16(double2 *A, int L1, int lm, const Sme
 #pragma unroll
       for (int jp = 0; jp < 4; ++jp) {            // stage s: butterfly k = jp mpp + kpp
         bfly4<false>(x[0][jp], x[1][jp], x[2][jp], x[3][jp]);
-        const int k = jp * mpp + kpp;
-        if (k != 0) {
-          x[1][jp] = cmul(x[1][jp], twid(sm, k * ts));
-          x[2][jp] = cmul(x[2][jp], twid(sm, 2 * k * ts));
-          x[3][jp] = cmul(x[3][jp], twid(sm, 3 * k * ts));
-        }
+        double2 v1, v2, v3;
+        tw3(sm, (jp * mpp + kpp) * ts, v1, v2, v3);
+        x[1][jp] = cmul(x[1][jp], v1);
+        x[2][jp] = cmul(x[2][jp], v2);
+        x[3][jp] = cmul(x[3][jp], v3);
       }
-      double2 w1 = zero2(), w2 = zero2(), w3 = zero2();
-      if (kpp != 0) { w1 = twid(sm, kpp * tsp); w2 = twid(sm, 2 * kpp * tsp); w3 = twid(sm, 3 * kpp * tsp); }
+      double2 w1, w2, w3;
+      tw3(sm, kpp * tsp, w1, w2, w3);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {               // stage s-1: butterfly k = kpp in group 4g + j
         bfly4<false>(x[j][0], x[j][1], x[j][2], x[j][3]);
-        if (kpp != 0) {
-          x[j][1] = cmul(x[j][1], w1);
-          x[j][2] = cmul(x[j][2], w2);
-          x[j][3] = cmul(x[j][3], w3);
-        }
+        x[j][1] = cmul(x[j][1], w1);
+        x[j][2] = cmul(x[j][2], w2);
+        x[j][3] = cmul(x[j][3], w3);
       }
     } else {
-      double2 w1 = zero2(), w2 = zero2(), w3 = zero2();
-      if (kpp != 0) { w1 = twid(sm, kpp * tsp); w2 = twid(sm, 2 * kpp * tsp); w3 = twid(sm, 3 * kpp * tsp); }
+      double2 w1, w2, w3;
+      tw3(sm, kpp * tsp, w1, w2, w3);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {               // DIT stage s-1
-        if (kpp != 0) {
-          x[j][1] = cmulc(x[j][1], w1);
-          x[j][2] = cmulc(x[j][2], w2);
-          x[j][3] = cmulc(x[j][3], w3);
-        }
+        x[j][1] = cmulc(x[j][1], w1);
+        x[j][2] = cmulc(x[j][2], w2);
+        x[j][3] = cmulc(x[j][3], w3);
         bfly4<true>(x[j][0], x[j][1], x[j][2], x[j][3]);
       }
 #pragma unroll
       for (int jp = 0; jp < 4; ++jp) {            // DIT stage s
-        const int k = jp * mpp + kpp;
-        if (k != 0) {
-          x[1][jp] = cmulc(x[1][jp], twid(sm, k * ts));
-          x[2][jp] = cmulc(x[2][jp], twid(sm, 2 * k * ts));
-          x[3][jp] = cmulc(x[3][jp], twid(sm, 3 * k * ts));
-        }
+        double2 v1, v2, v3;
+        tw3(sm, (jp * mpp + kpp) * ts, v1, v2, v3);
+        x[1][jp] = cmulc(x[1][jp], v1);
+        x[2][jp] = cmulc(x[2][jp], v2);
+        x[3][jp] = cmulc(x[3][jp], v3);
         bfly4<true>(x[0][jp], x[1][jp], x[2][jp], x[3][jp]);
       }
     }
@@ -1207,64 +1209,63 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   const double2 *Y = sm.A;      // output buffer of the last operator application
 
   if (rr0 > 0.0 && METHOD == TSF_BICGSTAB) {
+    // One BiCGSTAB iteration = four operator applications, h = 0..3: phat = P^{-1} p,
+    // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
+    // and geometry are selected per h) so the hot loop's code stays small for the instruction
+    // cache; the vector work before/after each application is dispatched on h.
     double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
-    for (int it = 0;; ++it) {
-      // Phase A: p = r + beta (p - omega v); phat = P^{-1} p; v = A phat; r^.v
-      if (it == 0) {
-        TSF_FOR_E(npc) { sm.A[pidx(e)] = R[e]; }
+    TSF_FOR_E(npc) { sm.A[pidx(e)] = R[e]; }     // p_0 = r_0
+    bool done = false;
+    for (int h = 0; !done; h = (h + 1) & 3) {
+      const bool isP = !(h & 1);
+      if (isP && !prec) {
+        Y = sm.A;
       } else {
-        batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
-                       [&](int e, T3 &t) {
-                         const double2 pv = caxpy(beta, caxpy(-omega, t.b, t.c), t.a);
-                         PV[e] = pv;
-                         sm.A[pidx(e)] = pv;
-                       });
+        __syncthreads();
+        const SpecOp op = isP ? opP : opA;
+        const Geo g = isP ? gp : ge;
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
       }
-      __syncthreads();
-      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
-      TSF_FOR_E(npc) {
-        const double2 ph = Y[pidx(e)];
-        PH[e] = ph;
-        sm.A[pidx(e)] = ph;
-        sm.A[pidx(e + npc)] = zero2();
+      if (isP) {
+        // h = 0: phat = Y; h = 2: shat = Y.  Either becomes the (padded) input of A.
+        double2 *const Dst = h == 0 ? PH : SH;
+        TSF_FOR_E(npc) {
+          const double2 z = Y[pidx(e)];
+          Dst[e] = z;
+          sm.A[pidx(e)] = z;
+          sm.A[pidx(e + npc)] = zero2();
+        }
+        continue;
       }
-      __syncthreads();
-      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
-      double d[1] = {0.0};
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; }, [&](int e, T1 &t) {
-        const double2 v = Y[pidx(e)];
-        VV[e] = v;
-        d[0] += cdot(t.a, v);
-      });
-      csum<C, 1>(d, sm, xs);
-      if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      alpha = rho / d[0];
-      // Phase B: s = r - alpha v; half-step exit on ||s||
-      double ss[1] = {0.0};
-      batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = VV[e]; t.b = R[e]; }, [&](int e, T2 &t) {
-        const double2 s = caxpy(-alpha, t.a, t.b);
-        S[e] = s;
-        sm.A[pidx(e)] = s;
-        ss[0] += cdot(s, s);
-      });
-      csum<C, 1>(ss, sm, xs);
-      if (sqrt(ss[0]) < P.tol * rn0) {
-        batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = PH[e]; t.b = X[e]; },
-                       [&](int e, T2 &t) { X[e] = caxpy(alpha, t.a, t.b); });
-        hs += 1;
-        relres = sqrt(ss[0]) / rn0;
-        break;
+      if (h == 1) {
+        // v = Y; alpha = rho / (r^.v); s = r - alpha v; half-step exit on ||s||
+        double d[1] = {0.0};
+        batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; }, [&](int e, T1 &t) {
+          const double2 v = Y[pidx(e)];
+          VV[e] = v;
+          d[0] += cdot(t.a, v);
+        });
+        csum<C, 1>(d, sm, xs);
+        if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        alpha = rho / d[0];
+        double ss[1] = {0.0};
+        batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = VV[e]; t.b = R[e]; }, [&](int e, T2 &t) {
+          const double2 s = caxpy(-alpha, t.a, t.b);
+          S[e] = s;
+          sm.A[pidx(e)] = s;
+          ss[0] += cdot(s, s);
+        });
+        csum<C, 1>(ss, sm, xs);
+        if (sqrt(ss[0]) < P.tol * rn0) {
+          batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = PH[e]; t.b = X[e]; },
+                                 [&](int e, T2 &t) { X[e] = caxpy(alpha, t.a, t.b); });
+          hs += 1;
+          relres = sqrt(ss[0]) / rn0;
+          break;
+        }
+        continue;
       }
-      //          shat = P^{-1} s; t = A shat; t.s, t.t
-      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
-      TSF_FOR_E(npc) {
-        const double2 sh = Y[pidx(e)];
-        SH[e] = sh;
-        sm.A[pidx(e)] = sh;
-        sm.A[pidx(e + npc)] = zero2();
-      }
-      __syncthreads();
-      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+      // h == 3: t = Y; omega = t.s / t.t; x += alpha phat + omega shat; r = s - omega t
       double tt[2] = {0.0, 0.0};
       batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = S[e]; }, [&](int e, T1 &ts) {
         const double2 t = Y[pidx(e)];
@@ -1274,7 +1275,6 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       csum<C, 2>(tt, sm, xs);
       if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       omega = tt[0] / tt[1];
-      // Phase C: x += alpha phat + omega shat; r = s - omega t; r^.r, r.r
       double rr[2] = {0.0, 0.0};
       batched<(TSF_BATCH > 2 ? 2 : TSF_BATCH), T5>(npc, [&](int e, T5 &t) { t.a = X[e]; t.b = SH[e]; t.c = PH[e]; t.d = S[e]; t.f = RH[e]; },
                      [&](int e, T5 &t) {
@@ -1293,6 +1293,13 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
       beta = (rr[0] / rho) * (alpha / omega);
       rho = rr[0];
+      // next p = r + beta (p - omega v) into A
+      batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
+                             [&](int e, T3 &t) {
+                               const double2 pv = caxpy(beta, caxpy(-omega, t.b, t.c), t.a);
+                               PV[e] = pv;
+                               sm.A[pidx(e)] = pv;
+                             });
     }
   } else if (rr0 > 0.0 && METHOD == TSF_PCGS) {
     // Preconditioned CGS (the paper's PCGS; MATLAB pcgs), right-preconditioned:

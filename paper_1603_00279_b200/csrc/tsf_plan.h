@@ -63,7 +63,7 @@ struct Plan {
   int32_t vsmem = 0;    // Krylov vectors of a CTA's chunk resident in SMEM (else HBM)
   int32_t staged = 0;   // cross-CTA step staged through SMEM buffers B (staging) and O (output)
   int32_t resident = 0; // per-instance constant tables cached in SMEM (small local length)
-  int32_t fuse_min = 16 * kThreads;
+  int32_t fuse_min = 1024;   // radix-16 passes from L1 = 1024 (measured, tools/fft_ubench.cu)
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;

@@ -26,7 +26,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP64 precond-Krylov iters/s & time levels/s at N=2^14; achieved HBM GB/s"
-KRYLOV_UNITS = {"bicgstab": 26, "cgnr": 19, "pcgs": 24}   # SURVEY 8(d)-style streamed units per iteration
+KRYLOV_UNITS = {"bicgstab": 26, "cgnr": 19, "pcgs": 24, "gsf": 26}   # SURVEY 8(d)-style streamed units per iteration
+GSF_UNITS_PER_LEVEL = 20   # GSF level: 5 applications x (input + output + 2-unit spectrum table)
 
 
 def peaks():
@@ -103,6 +104,8 @@ def algorithmic_bytes(n, M, iters_half_rows, method, src_units):
     for row in iters_half_rows:
         for j in range(M):
             total += 8.0 * n * (j + 3 + src_units + 8) + 8.0 * n * units * (row[j] / 2.0)
+            if method == "gsf" and j >= 1:
+                total += 8.0 * n * GSF_UNITS_PER_LEVEL
     return total
 
 
@@ -216,7 +219,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "cgnr", "pcgs"])
+    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "cgnr", "pcgs", "gsf"])
     ap.add_argument("--precond", default="strang", choices=["strang", "tchan", "none"])
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")

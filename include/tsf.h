@@ -56,7 +56,12 @@ extern "C" {
 
 /* TSF_PCGS: preconditioned CGS, the paper's own Krylov method (MATLAB pcgs, P:778-779,
  * P:917-925), right-preconditioned so the stopping test uses the unpreconditioned residual. */
-typedef enum { TSF_BICGSTAB = 0, TSF_CGNR = 1, TSF_PCGS = 2 } tsf_method;
+/* TSF_GSF: NEXT-2, the constant-coefficient path of alg2: level 0 by BiCGSTAB, levels
+ * j >= 1 by u = A^{-1} g through the Gohberg-Semencul formula (alg1x) built
+ * at tsf_init from A x = e_1, A y = e_n (eq3.4) solved by BiCGSTAB.  Requires gamma, d+, d- to
+ * be the same at every level (else TSF_E_ARG).  Per-level stats: iterations 0, relres = the
+ * true residual ||A u - g|| / ||g||. */
+typedef enum { TSF_BICGSTAB = 0, TSF_CGNR = 1, TSF_PCGS = 2, TSF_GSF = 3 } tsf_method;
 typedef enum { TSF_STRANG = 0, TSF_TCHAN = 1, TSF_NOPREC = 2 } tsf_precond;
 typedef enum { TSF_SRC_ZERO = 0, TSF_SRC_SEPARABLE = 1, TSF_SRC_TABLE = 2 } tsf_src_kind;
 

@@ -18,7 +18,7 @@ TSF_OK = 0
 TSF_W_MAXIT = 1
 ERRORS = {-1: "TSF_E_ARG", -2: "TSF_E_WORKSPACE", -3: "TSF_E_CUDA", -4: "TSF_E_SINGULAR_PREC",
           -5: "TSF_E_BREAKDOWN", -6: "TSF_E_DIVERGED", -7: "TSF_E_STATE"}
-BICGSTAB, CGNR, PCGS = 0, 1, 2
+BICGSTAB, CGNR, PCGS, GSF = 0, 1, 2, 3
 STRANG, TCHAN, NOPREC = 0, 1, 2
 SRC_ZERO, SRC_SEPARABLE, SRC_TABLE = 0, 1, 2
 

@@ -247,15 +247,65 @@ __global__ void k_dbg_spectra(DevParams P, int b, int64_t j, double2 *lamA, doub
 }
 
 // ---------------------------------------------------------------------- launch helpers
-cudaError_t launch_solve(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) {
+cudaError_t launch_solve(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, int32_t mode = 0) {
   switch (pl.C) {
-    case 1: return launch_solve_c<1>(pl, dp, nlev, st);
-    case 2: return launch_solve_c<2>(pl, dp, nlev, st);
-    case 4: return launch_solve_c<4>(pl, dp, nlev, st);
-    case 8: return launch_solve_c<8>(pl, dp, nlev, st);
-    case 16: return launch_solve_c<16>(pl, dp, nlev, st);
+    case 1: return launch_solve_c<1>(pl, dp, nlev, st, mode);
+    case 2: return launch_solve_c<2>(pl, dp, nlev, st, mode);
+    case 4: return launch_solve_c<4>(pl, dp, nlev, st, mode);
+    case 8: return launch_solve_c<8>(pl, dp, nlev, st, mode);
+    case 16: return launch_solve_c<16>(pl, dp, nlev, st, mode);
   }
   return cudaErrorInvalidValue;
+}
+
+// NEXT-2: 2n circulant embeddings (R-emb) of the four triangular Toeplitz factors of the
+// Gohberg-Semencul formula from x = A^{-1} e_1 (V_GX) and y = A^{-1} e_n (V_GY),
+// natural element e stored at perm_pos(n, C, e):
+//   k = 0  R_p^0 upper, first row [0, x_{n-1}, .., x_1]   c[n+t] = x_t      (t = 1..n-1)
+//   k = 1  R_p   upper, first row [y_{n-1}, .., y_0]      c[0] = y_{n-1}, c[n+t] = y_{t-1}
+//   k = 2  L_p^0 lower, first col [0, y_0, .., y_{n-2}]   c[m] = y_{m-1}    (m = 1..n-1)
+//   k = 3  L_p   lower, first col [x_0, .., x_{n-1}]      c[m] = x_m        (m < n)
+// and 1/xi_0 = 1/x_0 into par[7].
+__global__ void k_gsf_cols(DevParams P, int b0, int nb, int k, double2 *emb) {
+  const int64_t n = P.n;
+  const int64_t total = int64_t(nb) * 2 * n;
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int bb = int(id / (2 * n));
+    const int64_t m = id % (2 * n);
+    const Inst I = inst_view(P, b0 + bb);
+    const double *x = I.vec + int64_t(V_GX) * n, *y = I.vec + int64_t(V_GY) * n;
+    auto X = [&](int64_t e) { return x[perm_pos(n, P.C, e)]; };
+    auto Y = [&](int64_t e) { return y[perm_pos(n, P.C, e)]; };
+    double c = 0.0;
+    if (k == 0) c = (m > n) ? X(m - n) : 0.0;
+    else if (k == 1) c = (m == 0) ? Y(n - 1) : ((m > n) ? Y(m - n - 1) : 0.0);
+    else if (k == 2) c = (m >= 1 && m < n) ? Y(m - 1) : 0.0;
+    else c = (m < n) ? X(m) : 0.0;
+    emb[id] = make_double2(c, 0.0);
+    if (k == 0 && m == 0) I.par[7] = 1.0 / X(0);
+  }
+}
+
+// spectrum (natural bins 0..n of a length-2n transform) -> task order table k of I.gsf
+__global__ void k_gsf_scatter(DevParams P, int b0, int nb, int k, const double2 *spec) {
+  const int64_t n = P.n;
+  const int C = P.C;
+  const int64_t total = int64_t(nb) * (n + 1);
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int bb = int(id / (n + 1));
+    const int64_t idx = id % (n + 1);
+    Inst I = inst_view(P, b0 + bb);
+    int64_t bin = n;
+    if (idx < n) {
+      const int np = P.npe;
+      const int i = int(idx % np), ab = int((idx / np) % 2), k2 = int((idx / (2 * np)) % C);
+      const int r = int(idx / (2 * np * C));
+      bin = task_bin(P.L1e, C, r, i, k2, ab);
+    }
+    I.gsf[int64_t(k) * (n + 1) + idx] = spec[int64_t(bb) * 2 * n + bin];
+  }
 }
 
 cudaError_t launch_dbg_apply(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
@@ -406,7 +456,7 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
     const tsf_problem &q = p[b];
     InstTables T;
     inst_tables(q, &T);
-    double par[8] = {T.sigma, q.beta, 0.0, T.kappa, T.h, T.tau, 0.0, 0.0};
+    double par[16] = {T.sigma, q.beta, 0.0, T.kappa, T.h, T.tau, 0.0, 0.0};
     CKH(cudaMemcpy(inst_ptr(h, b, pl.o_par), par, sizeof(par), cudaMemcpyHostToDevice));
     CKH(cudaMemcpy(inst_ptr(h, b, pl.o_lev), T.lev.data(), T.lev.size() * 8, cudaMemcpyHostToDevice));
     CKH(cudaMemcpy(inst_ptr(h, b, pl.o_hwc), T.hwc.data(), T.hwc.size() * 8, cudaMemcpyHostToDevice));
@@ -465,6 +515,39 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
     CKH(cudaGetLastError());
   }
   CKH(cudaStreamSynchronize(st));
+
+  // NEXT-2 setup: x = A^{-1} e_1, y = A^{-1} e_n by BiCGSTAB (eq3.4), then the spectra of the
+  // four Gohberg-Semencul factors (same batched Stockham FFTs as the one-time spectra)
+  if (pl.method == TSF_GSF && M >= 2) {
+    CKH(launch_solve(pl, dp, 1, st, 1));
+    CKH(launch_solve(pl, dp, 1, st, 2));
+    for (int b0 = 0; b0 < B; b0 += pl.scratch_batch) {
+      const int nb = std::min(pl.scratch_batch, B - b0);
+      double2 *bufA = reinterpret_cast<double2 *>(h->ws + pl.off_scratch);
+      double2 *bufB = bufA + int64_t(nb) * 3 * n;
+      int le = 0;
+      while ((int64_t(1) << le) < 2 * n) ++le;
+      for (int k = 0; k < 4; ++k) {
+        k_gsf_cols<<<grid_for(int64_t(nb) * 2 * n), 256, 0, st>>>(dp, b0, nb, k, bufA);
+        double2 *src = bufA, *dst = bufB;
+        for (int ps = 0; ps < le; ++ps) {
+          k_stockham<<<grid_for(int64_t(nb) * n), 256, 0, st>>>(src, dst, 2 * n, ps, nb, tw, int(2 * n));
+          std::swap(src, dst);
+        }
+        k_gsf_scatter<<<grid_for(int64_t(nb) * (n + 1)), 256, 0, st>>>(dp, b0, nb, k, src);
+      }
+      CKH(cudaGetLastError());
+    }
+    CKH(cudaStreamSynchronize(st));
+    for (int32_t b = 0; b < B; ++b) {
+      double par[16];
+      CKH(cudaMemcpy(par, inst_ptr(h, b, pl.o_par), sizeof(par), cudaMemcpyDeviceToHost));
+      if (par[8] < 0 || par[9] < 0 || !std::isfinite(par[7])) {
+        set_error("GSF setup (A x = e_1, A y = e_n) failed for instance " + std::to_string(b));
+        return bail(TSF_E_BREAKDOWN);
+      }
+    }
+  }
 
   // CUDA graph of one level step: fused solve kernel (1 level) + level counter advance
   {

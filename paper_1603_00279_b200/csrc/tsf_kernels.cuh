@@ -64,6 +64,7 @@ struct Inst {
   const double *lev, *hwc, *hwe, *scal, *basis, *ftab;
   double *vec, *hist;
   double2 *mul;          // per-level multiplier tables [n + n/2] (task order), HBM variant
+  double2 *gsf;          // NEXT-2: spectra of the 4 triangular GSF factors [4][n+1] (task order)
   int32_t *it, *st;
   double *rr;
 };
@@ -84,6 +85,7 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.vec = reinterpret_cast<double *>(base + P.o_vec);
   I.hist = reinterpret_cast<double *>(base + P.o_hist);
   I.mul = reinterpret_cast<double2 *>(base + P.o_mul);
+  I.gsf = reinterpret_cast<double2 *>(base + P.o_gsf);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
   I.st = reinterpret_cast<int32_t *>(base + P.o_st);
@@ -1064,6 +1066,28 @@ __device__ __forceinline__ void fill_mul(const DevParams &P, const Inst &I, int6
   }
 }
 
+// NEXT-2 (alg1x): product with one triangular Toeplitz factor of the Gohberg-Semencul
+// formula through its 2n circulant embedding.  The factor's spectrum table is multiplied raw:
+// eta = 0, mu = ppq = pmq = 1, c2 = qcorr = 0 make the Nyquist formula return the stored value
+// exactly.  k: 0 = R_p^0, 1 = R_p, 2 = L_p^0, 3 = L_p (tsf_capi.cu k_gsf_cols).
+__device__ __forceinline__ SpecOp make_gsf_op(const DevParams &P, const Inst &I, int k, uint32_t r,
+                                              const Smem &sm) {
+  SpecOp op;
+  op.lam = I.lwe;
+  op.sq = P.sq_e;
+  op.mul = I.gsf + int64_t(k) * (P.n + 1);
+  op.mul_sh = false;
+  op.pw = sm.mule != nullptr ? sm.pwe : nullptr;
+  op.nyq = op.mul[P.n];
+  op.np = P.npe;
+  op.rC = int(r) * P.C;
+  op.eta = 0.0; op.mu = 1.0; op.ppq = 1.0; op.pmq = 1.0; op.c2 = 0.0; op.qcorr = 0.0;
+  op.scale = P.scale_e;
+  op.conj = false;
+  op.div = false;
+  return op;
+}
+
 // ------------------------------------------------------------------------ vector storage
 // Krylov vectors of this CTA's chunk (npc = L1p complex values): SMEM slots when the plan
 // keeps them on chip (P.vsmem), else the instance's HBM vector block (permuted chunks).
@@ -1172,12 +1196,92 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
 
 // ------------------------------------------------------------------------ one level
 // All control flow is uniform over the cluster (every CTA reduces to identical scalars).
+// NEXT-2, alg2 for j >= 1 with constant coefficients: u^{j+1} = A^{-1} g^{j+1} by the
+// Gohberg-Semencul formula and alg1x:
+//   z1 = R_p^0 g, z2 = R_p g, z3 = L_p^0 z1, z4 = L_p z2, u = (z4 - z3) / xi_0,
+// each factor applied through its 2n circulant embedding (four fused FFT applications), then
+// the true residual ||A u - g|| / ||g|| (one more application) is stored as the level's relres.
+// g arrives in A[0..npc) (rhs_phase) with ||g||^2 local partial g2loc.
+template <int C, bool STG>
+__device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
+                                          int64_t j, uint32_t r, Xch &xs, double g2loc) {
+  const int npc = P.L1p;
+  const int64_t n = P.n;
+  const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
+  const Geo ge = geo_embed(P, sm);
+  double2 *G = V.R, *Z1 = V.S, *Z2 = V.PH, *X = V.X;
+  TSF_FOR_E(npc) { G[e] = sm.A[pidx(e)]; }
+  double g2[1] = {g2loc};
+  csum<C, 1>(g2, sm, xs);
+  const double inv_xi0 = I.par[7];
+  const double2 *Y;
+  // z1 = R_p^0 g, z2 = R_p g
+  for (int k = 0; k < 2; ++k) {
+    TSF_FOR_E(npc) {
+      sm.A[pidx(e)] = G[e];
+      sm.A[pidx(e + npc)] = zero2();
+    }
+    __syncthreads();
+    const SpecOp op = make_gsf_op(P, I, k, r, sm);
+    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs);
+    double2 *Z = k == 0 ? Z1 : Z2;
+    TSF_FOR_E(npc) { Z[e] = Y[pidx(e)]; }
+  }
+  // z3 = L_p^0 z1 (kept in X), z4 = L_p z2, u = (z4 - z3) / xi_0
+  for (int k = 2; k < 4; ++k) {
+    const double2 *Z = k == 2 ? Z1 : Z2;
+    TSF_FOR_E(npc) {
+      sm.A[pidx(e)] = Z[e];
+      sm.A[pidx(e + npc)] = zero2();
+    }
+    __syncthreads();
+    const SpecOp op = make_gsf_op(P, I, k, r, sm);
+    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs);
+    if (k == 2) {
+      TSF_FOR_E(npc) { X[e] = Y[pidx(e)]; }
+    } else {
+      TSF_FOR_E(npc) { X[e] = cscale(csub(Y[pidx(e)], X[e]), inv_xi0); }
+    }
+  }
+  // true residual of the level: ||A u - g|| / ||g||
+  TSF_FOR_E(npc) {
+    sm.A[pidx(e)] = X[e];
+    sm.A[pidx(e + npc)] = zero2();
+  }
+  __syncthreads();
+  const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
+  Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+  double rs[1] = {0.0};
+  TSF_FOR_E(npc) {
+    const double2 d = csub(Y[pidx(e)], G[e]);
+    rs[0] += cdot(d, d);
+  }
+  csum<C, 1>(rs, sm, xs);
+  const double relres = g2[0] > 0.0 ? sqrt(rs[0] / g2[0]) : 0.0;
+  // finalize as the Krylov levels: d^j = u^{j+1} - u^j, u^j <- u^{j+1}
+  double2 *Hj = reinterpret_cast<double2 *>(I.hist + j * n) + r * npc;
+  TSF_FOR_E(npc) {
+    const double2 x = X[e], u = V.U[e];
+    Hj[e] = csub(x, u);
+    V.U[e] = x;
+  }
+  if (r == 0 && threadIdx.x == 0) {
+    I.it[j] = 0;
+    I.rr[j] = relres;
+    I.st[j] = isfinite(relres) ? TSF_LEVEL_OK : TSF_LEVEL_DIVERGED;
+  }
+  __syncthreads();
+}
+
 // Views (carve-up, instance, vectors) are computed by every thread from the kernel's own
 // pointers, so the compiler keeps SMEM accesses as LDS/STS (a view copied through shared memory
 // turned them into generic LD/ST and was measured slower).
+// mode 0: level j of the scheme.  mode 1 / 2 (NEXT-2 setup, TSF_GSF): solve A x = e_1 / A y = e_n
+// (eq3.4) with the level-j operators and store the solution in V_GX / V_GY; no RHS,
+// history or statistics.
 template <int C, int METHOD, bool STG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
-                                            int64_t j, uint32_t r, Xch &xs) {
+                                            int64_t j, uint32_t r, Xch &xs, int mode = 0) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
@@ -1193,11 +1297,30 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   const long long tlev0 = clock64();
 #endif
 
-  double g2[1] = {rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, xs)};
+  double g2[1] = {0.0};
+  if (mode == 0) {
+    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, xs);
+  } else {
+    // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
+    const int64_t m = mode == 1 ? 0 : n / 2 - 1;
+    TSF_FOR_E(npc) {
+      const bool hit = (int64_t(r) == m % C) && (int64_t(e) == m / C);
+      const double2 g = hit ? (mode == 1 ? make_double2(1.0, 0.0) : make_double2(0.0, 1.0)) : zero2();
+      sm.A[pidx(e)] = g;
+      sm.A[pidx(e + npc)] = zero2();
+      g2[0] += cdot(g, g);
+    }
+  }
+  if constexpr (METHOD == TSF_GSF) {
+    if (mode == 0 && j >= 1) {
+      gsf_level<C, STG>(P, I, sm, V, j, r, xs, g2[0]);
+      return;
+    }
+  }
   TSF_FOR_E(npc) {
     const double2 g = sm.A[pidx(e)];
     R[e] = g;
-    if (METHOD == TSF_BICGSTAB) { RH[e] = g; PV[e] = g; }
+    if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
     if (METHOD == TSF_PCGS) RH[e] = g;
     X[e] = zero2();
   }
@@ -1208,7 +1331,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   double relres = 0.0;
   const double2 *Y = sm.A;      // output buffer of the last operator application
 
-  if (rr0 > 0.0 && METHOD == TSF_BICGSTAB) {
+  if (rr0 > 0.0 && (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF)) {
     // One BiCGSTAB iteration = four operator applications, h = 0..3: phat = P^{-1} p,
     // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
     // and geometry are selected per h) so the hot loop's code stays small for the instruction
@@ -1448,6 +1571,13 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       gam = zz[0];
     }
   }
+  if (mode != 0) {               // GSF setup: keep the solution of eq3.4
+    double2 *G = reinterpret_cast<double2 *>(I.vec + (mode == 1 ? V_GX : V_GY) * n) + r * npc;
+    TSF_FOR_E(npc) { G[e] = X[e]; }
+    if (r == 0 && threadIdx.x == 0) I.par[mode == 1 ? 8 : 9] = double(status == TSF_LEVEL_OK ? hs : -1 - status);
+    __syncthreads();
+    return;
+  }
   // finalize (alg1 step 3 result): d^j = u^{j+1} - u^j, u^j <- u^{j+1}
   double2 *Hj = reinterpret_cast<double2 *>(I.hist + j * n) + r * npc;
   batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = X[e]; t.b = V.U[e]; }, [&](int e, T2 &t) {
@@ -1471,7 +1601,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 // ------------------------------------------------------------------------ kernels
 template <int C, int METHOD, bool STG, bool VS>
 __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
-    k_solve(DevParams P, int32_t nlev, int32_t) {
+    k_solve(DevParams P, int32_t nlev, int32_t mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
@@ -1495,7 +1625,11 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   xinit<C>(sm);
   Xch xs;
   const int64_t j0 = *P.level;
-  for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs);
+  if (mode != 0) {               // NEXT-2 setup solve with the level-1 operators
+    level_solve<C, METHOD, STG>(P, I, sm, V, 1, r, xs, mode);
+  } else {
+    for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs);
+  }
   if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
 #ifdef TSF_PROFILE
   __syncthreads();
@@ -1582,7 +1716,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
 // ------------------------------------------------------------------------ launch API
 // Implemented per cluster size in tsf_solve_c<C>.cu (parallel compilation).
 template <int C>
-cudaError_t launch_solve_c(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st);
+cudaError_t launch_solve_c(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, int32_t mode);
 template <int C>
 cudaError_t launch_dbg_apply_c(const Plan &pl, const DevParams &dp, int b, int64_t j, int which,
                                const double *in, double *out, cudaStream_t st, int32_t reps);
@@ -1617,9 +1751,9 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
 #define TSF_STG_OF(CC, pl) ((CC) > 1 && (pl).staged)
 #define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
   template <>                                                                                   \
-  cudaError_t launch_solve_c<CC>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st) { \
+  cudaError_t launch_solve_c<CC>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, \
+                                 int32_t z) {                                                   \
     const int g = pl.B * CC;                                                                    \
-    const int32_t z = 0;                                                                        \
     constexpr bool S1 = (CC) > 1;                                                               \
     const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
     if (pl.method == TSF_BICGSTAB) {                                                            \
@@ -1627,6 +1761,12 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
       if (stg) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1, false>, pl, g, st, dp, nlev, z); \
       if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, CC == 1>, pl, g, st, dp, nlev, z); \
       return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, false>, pl, g, st, dp, nlev, z);   \
+    }                                                                                           \
+    if (pl.method == TSF_GSF) {                                                                 \
+      if (stg && vs) return launch_cluster(k_solve<CC, TSF_GSF, S1, true>, pl, g, st, dp, nlev, z); \
+      if (stg) return launch_cluster(k_solve<CC, TSF_GSF, S1, false>, pl, g, st, dp, nlev, z);    \
+      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_GSF, false, CC == 1>, pl, g, st, dp, nlev, z); \
+      return launch_cluster(k_solve<CC, TSF_GSF, false, false>, pl, g, st, dp, nlev, z);          \
     }                                                                                           \
     if (pl.method == TSF_PCGS) {                                                                \
       if (stg && vs) return launch_cluster(k_solve<CC, TSF_PCGS, S1, true>, pl, g, st, dp, nlev, z); \

@@ -85,7 +85,26 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
         (p[0].src_kind == TSF_SRC_SEPARABLE && p[b].K != p[0].K))
       return fail("instance %g: all instances must share n, M, source kind and K", b);
   }
-  if (s->method != TSF_BICGSTAB && s->method != TSF_CGNR && s->method != TSF_PCGS) return fail("unknown method %g", s->method);
+  if (s->method != TSF_BICGSTAB && s->method != TSF_CGNR && s->method != TSF_PCGS && s->method != TSF_GSF) return fail("unknown method %g", s->method);
+  if (s->method == TSF_GSF) {
+    // alg2 / eqgux: A is level-invariant for j >= 1 only with constant coefficients
+    for (int32_t b = 0; b < B; ++b) {
+      const tsf_problem &q = p[b];
+      std::vector<double> t(static_cast<size_t>(q.M));
+      sample_points(q, nullptr, t.data());
+      bool ok = true;
+      const double g0 = coef(q.gamma_t, q.gamma_fn, q.coef_ctx, 0, t[0], &ok);
+      const double p0 = coef(q.dplus_t, q.dplus_fn, q.coef_ctx, 0, t[0], &ok);
+      const double m0 = coef(q.dminus_t, q.dminus_fn, q.coef_ctx, 0, t[0], &ok);
+      for (int64_t j = 1; j < q.M; ++j)
+        if (coef(q.gamma_t, q.gamma_fn, q.coef_ctx, j, t[size_t(j)], &ok) != g0 ||
+            coef(q.dplus_t, q.dplus_fn, q.coef_ctx, j, t[size_t(j)], &ok) != p0 ||
+            coef(q.dminus_t, q.dminus_fn, q.coef_ctx, j, t[size_t(j)], &ok) != m0)
+          return fail("method GSF needs constant gamma, d+, d- (alg2, P:863); instance %g varies at level %g",
+                      double(b), double(j));
+    }
+    if (s->precond == TSF_NOPREC) return fail("method GSF solves eq3.4 with a preconditioner (eqx2xzz, P:893)");
+  }
   if (s->precond != TSF_STRANG && s->precond != TSF_TCHAN && s->precond != TSF_NOPREC)
     return fail("unknown preconditioner %g", s->precond);
   if (!(s->tol > 0.0)) return fail("tol=%g must be > 0", s->tol);
@@ -174,7 +193,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.off_inst = o;
   // per-instance block
   size_t q = 0;
-  P.o_par = q;   q = up(q + 64);
+  P.o_par = q;   q = up(q + 128);
   P.o_omega = q; q = up(q + size_t(n + 2) * 8);
   P.o_lwe = q;   q = up(q + size_t(n + 1) * 16);
   P.o_lwp = q;   q = up(q + size_t(n / 2 + 1) * 16);
@@ -190,6 +209,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.o_rr = q;    q = up(q + size_t(P.M) * 8);
   P.o_st = q;    q = up(q + size_t(P.M) * 4);
   P.o_mul = q;   q = up(q + size_t(n + n / 2) * 16);
+  P.o_gsf = q;   q = up(q + (s->method == TSF_GSF ? size_t(4) * size_t(n + 1) * 16 : 0));
   P.stride = q;
   P.total = P.off_inst + P.stride * size_t(B);
   *pl = P;
@@ -307,7 +327,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.o_par = pl.o_par; d.o_omega = pl.o_omega; d.o_lwe = pl.o_lwe; d.o_lwp = pl.o_lwp;
   d.o_lev = pl.o_lev; d.o_hwc = pl.o_hwc; d.o_hwe = pl.o_hwe; d.o_scal = pl.o_scal;
   d.o_basis = pl.o_basis; d.o_ftab = pl.o_ftab; d.o_vec = pl.o_vec; d.o_hist = pl.o_hist;
-  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul;
+  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf;
   return d;
 }
 

@@ -15,7 +15,7 @@ namespace tsf {
 
 constexpr int kThreads = 256;          // threads per CTA
 constexpr int kMaxLocal = 8192;        // max complex elements of the local FFT (128 KiB)
-constexpr int kNumVec = 11;            // u, Krylov work vectors, phi copy
+constexpr int kNumVec = 13;            // u, Krylov work vectors, phi copy, GSF generators x, y
 constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^)
 constexpr int64_t kMaxSmem = 232448;   // opt-in dynamic shared memory per CTA (227 KiB)
 constexpr size_t kAlign = 256;
@@ -26,7 +26,7 @@ constexpr int kPadBuf = 0;             // XOR-swizzled transform buffers need no
 #endif
 
 // Vector slots inside the per-instance vector block (each n doubles).
-enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_PHI };
+enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_PHI, V_GX, V_GY };
 
 // Plain-old-data parameters handed to every kernel by value.
 struct DevParams {
@@ -51,7 +51,7 @@ struct DevParams {
   char *inst;                      // base of instance 0
   int64_t stride;                  // bytes between instances
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf;
 };
 
 struct Plan {
@@ -71,7 +71,7 @@ struct Plan {
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf;
 };
 
 // Per-instance host tables (all doubles).

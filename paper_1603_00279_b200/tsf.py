@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib as L
 from .inputs import Instance, manufactured_basis, manufactured_scal
 
-METHODS = {"bicgstab": L.BICGSTAB, "cgnr": L.CGNR, "pcgs": L.PCGS}
+METHODS = {"bicgstab": L.BICGSTAB, "cgnr": L.CGNR, "pcgs": L.PCGS, "gsf": L.GSF}
 PRECONDS = {"strang": L.STRANG, "tchan": L.TCHAN, "none": L.NOPREC}
 
 

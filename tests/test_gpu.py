@@ -181,6 +181,36 @@ def test_pcgs_parity_and_paper_iteration_range(cluster, precond):
         assert 5 <= it.min() / 2 and it.max() / 2 <= 11, it / 2
 
 
+@pytest.mark.parametrize("cluster", [1, 2, 16])
+def test_gsf_constant_coefficient_path_parity(cluster):
+    """NEXT-2 (alg2): level 0 by BiCGSTAB, levels j >= 1 by the Gohberg-Semencul
+    inverse (alg1x) built from A x = e_1, A y = e_n; C3-type coefficients and random
+    source.  Same 1e-9 parity bar as the Krylov path; the stored relres is the true residual."""
+    f = np.random.default_rng(160300279).standard_normal((16, 1024))
+    inst, p = pair(0.9, 1.9, 1024, 16, gamma=(O.CONST, 1.0), dplus=(O.CONST, 2.0), dminus=(O.CONST, 0.5),
+                   src="table", f_table=f)
+    s = tsf.Solver([inst], method="gsf", cluster=cluster)
+    U = run_levels(s, 16)[0]
+    assert max_rel(U, O.solve(p)) <= RTOL
+    it, rr, st = s.stats()
+    assert (st == 0).all() and (it[0, 1:] == 0).all() and it[0, 0] > 0 and rr[0, 1:].max() < 1e-9
+
+
+def test_gsf_c1_config_and_batch_parity():
+    rng = np.random.default_rng(11)
+    pairs = [pair(float(rng.uniform(0.2, 0.95)), float(rng.uniform(1.2, 1.9)), 256, 12,
+                  gamma=(O.CONST, float(rng.uniform(-1, 1))), dplus=(O.CONST, float(rng.uniform(0, 2))),
+                  dminus=(O.CONST, float(rng.uniform(0, 2)))) for _ in range(4)]
+    s = tsf.Solver([a for a, _ in pairs], method="gsf")
+    U = run_levels(s, 12)
+    for b, (_, p) in enumerate(pairs):
+        assert max_rel(U[b], O.solve(p)) <= RTOL
+    inst = config_c1()[0]
+    _, p = pair(0.5, 1.5, 64, 64, gamma=(O.CONST, 0.5))
+    s = tsf.Solver([inst], method="gsf")
+    assert max_rel(run_levels(s, 64)[0], O.solve(p)) <= RTOL
+
+
 @pytest.mark.parametrize("cluster", [1, 2, 4, 8, 16])
 def test_table_source_parity_every_cluster(cluster):
     f = np.random.default_rng(160300279).standard_normal((12, 1024))

@@ -79,6 +79,18 @@ def test_solver_settings_validated():
         tsf.plan([inst], cluster=16)          # n = 64 < 4 C^2
 
 
+def test_gsf_method_requires_constant_coefficients_and_a_preconditioner():
+    # NEXT-2 (alg2) is defined for gamma, d+- constant in time (eqgux)
+    ok = Instance(alpha=0.5, beta=1.5, n=64, M=4, gamma=const(0.5), dplus=const(1.0), dminus=const(1.0))
+    assert tsf.plan([ok], method="gsf").cluster == 1
+    var = Instance(alpha=0.5, beta=1.5, n=64, M=4, gamma=const(0.5), dplus=lambda t: 1.0 + t,
+                   dminus=const(1.0))
+    with pytest.raises(L.TsfError, match="constant"):
+        tsf.plan([var], method="gsf")
+    with pytest.raises(L.TsfError, match="preconditioner"):
+        tsf.plan([ok], method="gsf", precond="none")
+
+
 def test_planner_cluster_choices_and_workspace():
     c1 = tsf.plan(CONFIGS["C1"]())
     c3 = tsf.plan(config_c3())

@@ -1148,37 +1148,63 @@ struct T5 { double2 a, b, c, d, f; };
 template <int C, bool STG>
 __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
                                             const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
-                                            Xch &xs) {
+                                            double2 *Hsum, Xch &xs) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
+  TSF_PT0();
+  const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
+  const int64_t hstride = n / 2;  // double2 per history row
+  // history term kappa (e_j d^0 + sum_{s=1}^{j-1} chat_{j-s} d^s) into Hs (the X slot, zeroed after
+  // the RHS anyway): two elements per thread and HU rows per batch, all loads of a batch issued
+  // before the FMAs (HU x 2 loads in flight per thread; the sum streams j rows of the CTA chunk)
+  double2 *Hs = Hsum;
+  if (j >= 1) {
+    constexpr int HU = C == 1 ? 4 : 8;
+    for (int e0 = threadIdx.x; e0 < npc; e0 += 2 * kThreads) {
+      const int e1 = e0 + kThreads;
+      const bool has1 = e1 < npc;
+      const double wj = I.hwe[j];
+      double2 a0 = cscale(H[e0], wj), a1 = has1 ? cscale(H[e1], wj) : zero2();
+      double2 b0 = zero2(), b1 = zero2();
+      int64_t s = 1;
+      for (; s + HU - 1 <= j - 1; s += HU) {
+        double2 v0[HU], v1[HU];
+        double w[HU];
+#pragma unroll
+        for (int u = 0; u < HU; ++u) {
+          v0[u] = H[(s + u) * hstride + e0];
+          v1[u] = has1 ? H[(s + u) * hstride + e1] : zero2();
+          w[u] = I.hwc[j - s - u];
+        }
+#pragma unroll
+        for (int u = 0; u < HU; u += 2) {
+          a0 = caxpy(w[u], v0[u], a0);
+          a1 = caxpy(w[u], v1[u], a1);
+          b0 = caxpy(w[u + 1], v0[u + 1], b0);
+          b1 = caxpy(w[u + 1], v1[u + 1], b1);
+        }
+      }
+      for (; s <= j - 1; ++s) {
+        const double w = I.hwc[j - s];
+        a0 = caxpy(w, H[s * hstride + e0], a0);
+        if (has1) a1 = caxpy(w, H[s * hstride + e1], a1);
+      }
+      Hs[e0] = cadd(a0, b0);
+      if (has1) Hs[e1] = cadd(a1, b1);
+    }
+  }
+  TSF_PACC(sm, PS_RHS_HIST);
   TSF_FOR_E(npc) {
     sm.A[pidx(e)] = U[e];
     sm.A[pidx(e + npc)] = zero2();
   }
   __syncthreads();
   const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs);
-  const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
-  const int64_t hstride = n / 2;  // double2 per history row
   double acc = 0.0;
-  TSF_PT0();
   TSF_FOR_E(npc) {
     double2 g = Y[pidx(e)];
-    if (j >= 1) {
-      double2 h0 = cscale(H[e], I.hwe[j]);
-      double2 h1 = zero2(), h2 = h1, h3 = h1;
-      int64_t s = 1;
-      for (; s + 3 <= j - 1; s += 4) {
-        const double2 d0 = H[s * hstride + e], d1 = H[(s + 1) * hstride + e];
-        const double2 d2 = H[(s + 2) * hstride + e], d3 = H[(s + 3) * hstride + e];
-        h0 = caxpy(I.hwc[j - s], d0, h0);
-        h1 = caxpy(I.hwc[j - s - 1], d1, h1);
-        h2 = caxpy(I.hwc[j - s - 2], d2, h2);
-        h3 = caxpy(I.hwc[j - s - 3], d3, h3);
-      }
-      for (; s <= j - 1; ++s) h0 = caxpy(I.hwc[j - s], H[s * hstride + e], h0);
-      g = csub(g, cadd(cadd(h0, h1), cadd(h2, h3)));
-    }
+    if (j >= 1) g = csub(g, Hs[e]);
     if (P.src_kind == TSF_SRC_SEPARABLE) {
       const double2 *Bs = reinterpret_cast<const double2 *>(I.basis) + r * npc;
       for (int k = 0; k < P.K; ++k) g = caxpy(I.scal[j * P.K + k], Bs[k * hstride + e], g);
@@ -1190,7 +1216,6 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
     sm.A[pidx(e + npc)] = zero2();
     acc += cdot(g, g);
   }
-  TSF_PACC(sm, PS_RHS_HIST);
   return acc;
 }
 
@@ -1299,7 +1324,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 
   double g2[1] = {0.0};
   if (mode == 0) {
-    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, xs);
+    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, V.X, xs);
   } else {
     // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
     const int64_t m = mode == 1 ? 0 : n / 2 - 1;
@@ -1707,7 +1732,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
   Xch xs;
   const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const double2 *U = reinterpret_cast<const double2 *>(I.vec + V_U * P.n) + r * npc;
-  rhs_phase<C, STG>(P, sm, I, geo_embed(P, sm), opB, j, r, U, xs);
+  double2 *Hs = reinterpret_cast<double2 *>(I.vec + V_X * P.n) + r * npc;
+  rhs_phase<C, STG>(P, sm, I, geo_embed(P, sm), opB, j, r, U, Hs, xs);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
   for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
   csync<C>();

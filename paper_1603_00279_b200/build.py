@@ -15,7 +15,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libtsf.so")
 PROF_LIB = os.path.join(LIBDIR, "libtsf_prof.so")
-SOURCES = ["tsf_plan.cpp", "tsf_capi.cu"] + [f"tsf_solve_c{c}.cu" for c in (1, 2, 4, 8, 16)]
+SOURCES = (["tsf_plan.cpp", "tsf_capi.cu"] + [f"tsf_solve_c{c}.cu" for c in (1, 2, 4, 8, 16)]
+           + [f"tsf_solve_c{c}_{m}.cu" for c in (1, 2, 4, 8, 16) for m in ("bicgstab", "cgnr", "pcgs", "gsf")])
 HEADERS = ["tsf_plan.h", "tsf_kernels.cuh", os.path.join("..", "..", "include", "tsf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -51,7 +52,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, var
         return lib
     os.makedirs(LIBDIR, exist_ok=True)
     extra = [f"-D{d}" for d in defines]
-    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose, profile, extra, variant), SOURCES))
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs])
     os.replace(lib + ".tmp", lib)

@@ -689,6 +689,7 @@ __device__ __forceinline__ void pair_self(double2 &Z, double2 la, double2 lb, do
 struct Geo {
   int L1, L, np, twL, tw2L;   // twL = twN/L (W_L factor), tw2L = twN/(2L)
   int l1;                     // log2(L1)
+  int lnp;                    // log2(np): task indices split by shifts, not integer division
   const int32_t *slot;
   const double2 *ctw;         // resident column twiddles W_L^{q k1(col)} [q ncol + col]
 };
@@ -758,7 +759,7 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   mbar_wait(mbB, ph);
   TSF_PACC(sm, PS_GATHER);
   for (int t = threadIdx.x; t < ncol; t += kThreads) {        // column DFT_C
-    const int ab = t / np, i = t - ab * np, colo = 2 * i + ab;
+    const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
     const int k1 = col_k1(L1, C, r, colo);
     double2 z[C];
 #pragma unroll
@@ -778,7 +779,7 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   TSF_PACC(sm, PS_COLF);
   // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1))
   for (int u = threadIdx.x; u < np * C; u += kThreads) {
-    const int k2 = u / np, i = u - k2 * np;
+    const int k2 = u >> g.lnp, i = u & (np - 1);
     const int pi = int(r) + i * C;
     if (pi != 0) {
       const int bin = pi + L1 * k2;
@@ -835,7 +836,7 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   {
     const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
     for (int t = threadIdx.x; t < ncol; t += kThreads) {      // inverse column DFT_C + push back
-      const int ab = t / np, i = t - ab * np, colo = 2 * i + ab;
+      const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
       const int k1 = col_k1(L1, C, r, colo);
       double2 z[C];
 #pragma unroll
@@ -986,6 +987,7 @@ __device__ __forceinline__ Geo geo_embed(const DevParams &P, const Smem &sm) {
   g.slot = P.slot_e;
   g.ctw = sm.ctwe;
   g.l1 = __ffs(g.L1) - 1;
+  g.lnp = __ffs(g.np) - 1;
   return g;
 }
 __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
@@ -994,6 +996,7 @@ __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
   g.slot = P.slot_p;
   g.ctw = sm.ctwp;
   g.l1 = __ffs(g.L1) - 1;
+  g.lnp = __ffs(g.np) - 1;
   return g;
 }
 
@@ -1059,7 +1062,8 @@ __device__ __forceinline__ void fill_mul(const DevParams &P, const Inst &I, int6
   const int np = P.npp;
   for (int u = threadIdx.x; u < L1p; u += kThreads) {
     const int64_t g = int64_t(r) * L1p + u;
-    const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+    const int lnp = __ffs(np) - 1;
+    const int i = u & (np - 1), ab = (u >> lnp) & 1, k2 = u >> (lnp + 1);
     const int bin = int(task_bin(L1p, C, int(r), i, k2, ab));
     const double2 v = pinv.eff(pinv.lam_idx(int(g), bin));
     if (res) sm.mulp[u] = v; else I.mul[P.n + g] = v;
@@ -1775,35 +1779,33 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
 
 // Staged exchange (STG) exists for C > 1 only.
 #define TSF_STG_OF(CC, pl) ((CC) > 1 && (pl).staged)
+// Solve-kernel launchers per (cluster size, method), each instantiated in its own translation unit
+// tsf_solve_c<C>_m<M>.cu (parallel compilation); launch_solve_c<C> dispatches on the method.
+template <int C, int METHOD>
+cudaError_t launch_solve_cm(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, int32_t mode);
+#define TSF_INSTANTIATE_METHOD(CC, MM)                                                          \
+  template <>                                                                                   \
+  cudaError_t launch_solve_cm<CC, MM>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, \
+                                      int32_t z) {                                              \
+    const int g = pl.B * CC;                                                                    \
+    constexpr bool S1 = (CC) > 1;                                                               \
+    const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
+    if (stg && vs) return launch_cluster(k_solve<CC, MM, S1, true>, pl, g, st, dp, nlev, z);    \
+    if (stg) return launch_cluster(k_solve<CC, MM, S1, false>, pl, g, st, dp, nlev, z);         \
+    if (vs && CC == 1) return launch_cluster(k_solve<CC, MM, false, CC == 1>, pl, g, st, dp, nlev, z); \
+    return launch_cluster(k_solve<CC, MM, false, false>, pl, g, st, dp, nlev, z);               \
+  }
 #define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
   template <>                                                                                   \
   cudaError_t launch_solve_c<CC>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, \
                                  int32_t z) {                                                   \
-    const int g = pl.B * CC;                                                                    \
-    constexpr bool S1 = (CC) > 1;                                                               \
-    const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
-    if (pl.method == TSF_BICGSTAB) {                                                            \
-      if (stg && vs) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1, true>, pl, g, st, dp, nlev, z); \
-      if (stg) return launch_cluster(k_solve<CC, TSF_BICGSTAB, S1, false>, pl, g, st, dp, nlev, z); \
-      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, CC == 1>, pl, g, st, dp, nlev, z); \
-      return launch_cluster(k_solve<CC, TSF_BICGSTAB, false, false>, pl, g, st, dp, nlev, z);   \
+    switch (pl.method) {                                                                        \
+      case TSF_BICGSTAB: return launch_solve_cm<CC, TSF_BICGSTAB>(pl, dp, nlev, st, z);         \
+      case TSF_CGNR: return launch_solve_cm<CC, TSF_CGNR>(pl, dp, nlev, st, z);                 \
+      case TSF_PCGS: return launch_solve_cm<CC, TSF_PCGS>(pl, dp, nlev, st, z);                 \
+      case TSF_GSF: return launch_solve_cm<CC, TSF_GSF>(pl, dp, nlev, st, z);                   \
     }                                                                                           \
-    if (pl.method == TSF_GSF) {                                                                 \
-      if (stg && vs) return launch_cluster(k_solve<CC, TSF_GSF, S1, true>, pl, g, st, dp, nlev, z); \
-      if (stg) return launch_cluster(k_solve<CC, TSF_GSF, S1, false>, pl, g, st, dp, nlev, z);    \
-      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_GSF, false, CC == 1>, pl, g, st, dp, nlev, z); \
-      return launch_cluster(k_solve<CC, TSF_GSF, false, false>, pl, g, st, dp, nlev, z);          \
-    }                                                                                           \
-    if (pl.method == TSF_PCGS) {                                                                \
-      if (stg && vs) return launch_cluster(k_solve<CC, TSF_PCGS, S1, true>, pl, g, st, dp, nlev, z); \
-      if (stg) return launch_cluster(k_solve<CC, TSF_PCGS, S1, false>, pl, g, st, dp, nlev, z);   \
-      if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_PCGS, false, CC == 1>, pl, g, st, dp, nlev, z); \
-      return launch_cluster(k_solve<CC, TSF_PCGS, false, false>, pl, g, st, dp, nlev, z);         \
-    }                                                                                           \
-    if (stg && vs) return launch_cluster(k_solve<CC, TSF_CGNR, S1, true>, pl, g, st, dp, nlev, z); \
-    if (stg) return launch_cluster(k_solve<CC, TSF_CGNR, S1, false>, pl, g, st, dp, nlev, z);   \
-    if (vs && CC == 1) return launch_cluster(k_solve<CC, TSF_CGNR, false, CC == 1>, pl, g, st, dp, nlev, z); \
-    return launch_cluster(k_solve<CC, TSF_CGNR, false, false>, pl, g, st, dp, nlev, z);         \
+    return cudaErrorInvalidValue;                                                               \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \

@@ -177,6 +177,7 @@ struct Smem {
   double *red;                       // push reductions: [2][16][4] CTA partials (double-buffered)
   uint64_t *mbar;                    // mbarriers: [0] exchange-in B, [1] exchange-back O, [2..3] red
   int fuse_min;                      // local FFTs of at least this length use radix-16 passes
+  int chunk;                         // column pairs per chunk of the unstaged column stage (B = chunk buffer)
   unsigned long long *prof;
 };
 
@@ -204,13 +205,15 @@ __device__ __forceinline__ int tw_lo_len(int L1e) { return L1e >= 64 ? 64 : L1e;
 
 __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, bool staged,
                                           bool resident, bool vsmem, unsigned long long *prof,
-                                          int fuse_min = 16 * kThreads) {
+                                          int fuse_min = 16 * kThreads, int chunk = 0, int C = 1) {
   Smem s = {};
   s.prof = prof;
   s.fuse_min = fuse_min;
+  s.chunk = chunk;
   double2 *c = reinterpret_cast<double2 *>(raw);
   s.A = c; c += L1e + kPadBuf * (L1e / 16);
   if (staged) { s.B = c; c += L1e; s.O = c; c += L1e + kPadBuf * (L1e / 16); }
+  else if (chunk > 0) { s.B = c; c += 2 * chunk * C; }
   if (resident) {
     s.twd = c; c += L1e;
     s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
@@ -860,82 +863,106 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   TSF_PACC(sm, PS_BAR3);
 }
 
-// C > 1 without a staging buffer (shared memory full): one thread per column pair keeps the
-// 2C values in registers across the barrier.  Requires np <= kThreads.
+// C > 1 without room for B and O (L1 = 8192, C5): the column stage in chunks of CP column
+// pairs through a chunk buffer Bc (layout Bc[q * 2CP + 2 il + ab], conflict-free column reads).
+// Per chunk: pull the rows of its columns from every CTA's A (DSMEM), column DFT_C, bin pairs,
+// inverse column DFT_C and push the results straight back into the owners' A at the same slots.
+// Slots of a column pair are read and written only by the pair's owner, so chunks need no
+// cluster barrier; the caller's barriers order the local FFTs before the first pull and every
+// push before the local inverse FFTs.
 template <int C>
-__device__ __noinline__ void cross_reg(double2 *A, const Geo &g, const SpecOp &op,
-                                       const double2 *__restrict__ tw, uint32_t r) {
-  double2 za[C], zb[C];
-  const int i = threadIdx.x;
-  const bool act = i < g.np;
-  const int pi = int(r) + i * C;
-  const bool pseudo = (pi == 0);
-  const int k1a = pseudo ? 0 : pi;
-  const int k1b = pseudo ? g.L1 / 2 : g.L1 - pi;
-  int sa = 0, sb = 0;
-  if (act) {
-    sa = pidx(dslot(k1a, g.l1));
-    sb = pidx(dslot(k1b, g.l1));
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-      const double2 *Aq = remote<C>(A, uint32_t(q));
-      za[q] = Aq[sa];
-      zb[q] = Aq[sb];
+__device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, const Geo &g, const SpecOp &op,
+                                              const double2 *__restrict__ tw, uint32_t r) {
+  const int L1 = g.L1, np = g.np, l1 = g.l1;
+  const int W = 2 * CP;                       // columns per chunk
+  for (int c0 = 0; c0 < np; c0 += CP) {
+    const int cp = np - c0 < CP ? np - c0 : CP;
+    // pull: item u -> (row q, chunk column col)
+    for (int u = threadIdx.x; u < C * 2 * cp; u += kThreads) {
+      const int q = u / (2 * cp), col = u - q * (2 * cp);
+      const int k1 = col_k1(L1, C, r, 2 * c0 + col);
+      Bc[q * W + col] = remote<C>(A, uint32_t(q))[pidx(dslot(k1, l1))];
     }
+    __syncthreads();
+    for (int col = threadIdx.x; col < 2 * cp; col += kThreads) {   // column DFT_C
+      const int k1 = col_k1(L1, C, r, 2 * c0 + col);
+      double2 z[C];
 #pragma unroll
-    for (int q = 1; q < C; ++q) {
-      za[q] = cmul(za[q], tw[q * k1a * g.twL]);
-      zb[q] = cmul(zb[q], tw[q * k1b * g.twL]);
+      for (int q = 0; q < C; ++q) z[q] = Bc[q * W + col];
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+      fft_reg<C, false>(z);
+#pragma unroll
+      for (int q = 0; q < C; ++q) Bc[q * W + col] = z[q];
     }
-    fft_reg<C, false>(za);
-    fft_reg<C, false>(zb);
-    if (!pseudo) {
-#pragma unroll
-      for (int k2 = 0; k2 < C; ++k2) {
-        const int bin = k1a + g.L1 * k2;
-        pair_apply(za[k2], zb[C - 1 - k2], op.get(k2, 0, i, bin),
-                        op.get(C - 1 - k2, 1, i, g.L - bin), tw[bin * g.tw2L], op.scale);
-      }
-    } else {
-#pragma unroll
-      for (int k2 = 0; k2 <= C / 2; ++k2) {
+    __syncthreads();
+    // bin pairs: item u = k2 * cp + il; (row k2, col (il,0)) <-> (row C-1-k2, col (il,1))
+    for (int u = threadIdx.x; u < C * cp; u += kThreads) {
+      const int k2 = u / cp, il = u - k2 * cp, i = c0 + il;
+      const int pi = int(r) + i * C;
+      if (pi != 0) {
+        const int bin = pi + L1 * k2;
+        double2 &za = Bc[k2 * W + 2 * il];
+        double2 &zb = Bc[(C - 1 - k2) * W + 2 * il + 1];
+        double2 a = za, b = zb;
+        pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
+                   op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
+        za = a;
+        zb = b;
+      } else {
         const int kk = (C - k2) % C;
-        const int bin = g.L1 * k2;
-        const double2 la = op.get(k2, 0, 0, bin);
-        if (kk == k2) {
-          const double2 lb = (k2 == 0) ? op.nyquist(g.L) : la;
-          pair_self(za[k2], la, lb, tw[bin * g.tw2L], op.scale);
-        } else {
-          pair_apply(za[k2], za[kk], la, op.get(kk, 0, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
+        if (k2 <= C / 2) {                      // column 0: bins L1 k2 <-> L1 (C - k2)
+          const int bin = L1 * k2;
+          const double2 la = op.get(k2, 0, 0, bin);
+          const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
+          double2 &za = Bc[k2 * W];
+          if (kk == k2) {
+            double2 a = za;
+            pair_self(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
+            za = a;
+          } else {
+            double2 &zb = Bc[kk * W];
+            double2 a = za, b = zb;
+            pair_apply(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
+            za = a;
+            zb = b;
+          }
+        }
+        const int km = C - 1 - k2;
+        if (k2 < (C + 1) / 2) {                 // column L1/2: bins L1/2 + L1 k2 <-> k2' = C-1-k2
+          const int bin = L1 / 2 + L1 * k2;
+          const double2 la = op.get(k2, 1, 0, bin);
+          const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
+          double2 &za = Bc[k2 * W + 1];
+          if (km == k2) {
+            double2 a = za;
+            pair_self(a, la, la, w, op.scale);
+            za = a;
+          } else {
+            double2 &zb = Bc[km * W + 1];
+            double2 a = za, b = zb;
+            pair_apply(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
+            za = a;
+            zb = b;
+          }
         }
       }
-#pragma unroll
-      for (int k2 = 0; k2 < (C + 1) / 2; ++k2) {
-        const int kk = C - 1 - k2;
-        const int bin = g.L1 / 2 + g.L1 * k2;
-        const double2 la = op.get(k2, 1, 0, bin);
-        if (kk == k2) pair_self(zb[k2], la, la, tw[bin * g.tw2L], op.scale);
-        else pair_apply(zb[k2], zb[kk], la, op.get(kk, 1, 0, g.L - bin), tw[bin * g.tw2L], op.scale);
-      }
     }
-    fft_reg<C, true>(za);
-    fft_reg<C, true>(zb);
+    __syncthreads();
+    for (int col = threadIdx.x; col < 2 * cp; col += kThreads) {   // inverse column DFT_C + push
+      const int k1 = col_k1(L1, C, r, 2 * c0 + col);
+      double2 z[C];
 #pragma unroll
-    for (int q = 1; q < C; ++q) {
-      za[q] = cmulc(za[q], tw[q * k1a * g.twL]);
-      zb[q] = cmulc(zb[q], tw[q * k1b * g.twL]);
+      for (int q = 0; q < C; ++q) z[q] = Bc[q * W + col];
+      fft_reg<C, true>(z);
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      const int s = pidx(dslot(k1, l1));
+#pragma unroll
+      for (int q = 0; q < C; ++q) remote<C>(A, uint32_t(q))[s] = z[q];
     }
+    __syncthreads();                            // Bc is refilled by the next chunk
   }
-  csync<C>();
-  if (act) {
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-      double2 *Aq = remote<C>(A, uint32_t(q));
-      Aq[sa] = za[q];
-      Aq[sb] = zb[q];
-    }
-  }
-  csync<C>();
 }
 
 // y = op(x) for the CTA's local data already in A[0..L1) (natural order, visible).
@@ -966,7 +993,9 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
     } else {
       csync<C>();                // every local transform done before remote gathers
       TSF_PACC(sm, PS_BAR1);
-      cross_reg<C>(sm.A, g, op, tw, r);
+      cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r);
+      csync<C>();                // every push landed before the local inverse transforms
+      TSF_PACC(sm, PS_BAR3);
     }
     TSF_PTR();
   }
@@ -1641,9 +1670,9 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   __shared__ unsigned long long prof_s[32];
   if (threadIdx.x < 32) prof_s[threadIdx.x] = 0;
   __syncthreads();
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min, P.chunk, P.C);
 #else
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min, P.chunk, P.C);
 #endif
   const Vecs V = vec_view<VS>(P, I, sm, r);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
@@ -1682,9 +1711,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
   __shared__ unsigned long long prof_s[32];
   if (threadIdx.x < 32) prof_s[threadIdx.x] = 0;
   __syncthreads();
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, prof_s, P.fuse_min, P.chunk, P.C);
 #else
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min, P.chunk, P.C);
 #endif
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int npc = P.L1p;
@@ -1726,7 +1755,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
-  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min);
+  const Smem sm = smem_view(smem_raw, P.L1e, P.L1p, P.staged != 0, P.resident != 0, P.vsmem != 0, P.prof, P.fuse_min, P.chunk, P.C);
   load_constants(P, I.lwe, P.precond != TSF_NOPREC ? I.lwp : nullptr, sm, r);
   const int64_t j = *P.level;
   const int npc = P.L1p;

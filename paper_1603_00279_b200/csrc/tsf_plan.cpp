@@ -174,6 +174,13 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
     if (const char *ev = std::getenv("TSF_VSMEM")) P.vsmem = (with <= kMaxSmem) ? std::atoi(ev) : 0;
   }
   P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem);
+  if (C > 1 && !P.staged) {      // chunk buffer: the largest power-of-two pair count that fits
+    int chunk = P.npe;
+    while (chunk > 1 && P.smem + int64_t(2) * chunk * C * 16 > kMaxSmem) chunk /= 2;
+    if (const char *ec = std::getenv("TSF_CHUNK")) chunk = std::min(chunk, std::max(1, std::atoi(ec)));
+    P.chunk = chunk;
+    P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem, int64_t(2) * chunk * C);
+  }
   if (const char *ef = std::getenv("TSF_FUSE_MIN")) P.fuse_min = std::atoi(ef);
 
   // shared tables
@@ -308,7 +315,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.n = pl.n; d.M = pl.M; d.B = pl.B; d.C = pl.C; d.K = pl.K; d.src_kind = pl.src_kind;
   d.method = pl.method; d.precond = pl.precond; d.maxit = pl.maxit;
   d.L1e = pl.L1e; d.L1p = pl.L1p; d.npe = pl.npe; d.npp = pl.npp;
-  d.staged = pl.staged; d.resident = pl.resident; d.vsmem = pl.vsmem; d.fuse_min = pl.fuse_min;
+  d.staged = pl.staged; d.resident = pl.resident; d.vsmem = pl.vsmem; d.fuse_min = pl.fuse_min; d.chunk = pl.chunk;
   d.tol = pl.tol;
   d.scale_e = 1.0 / (4.0 * double(pl.n));
   d.scale_p = 1.0 / (4.0 * double(pl.n / 2));

@@ -36,6 +36,7 @@ struct DevParams {
   int32_t staged, resident;        // exchange / SMEM-table modes (see Plan)
   int32_t vsmem;                   // Krylov vectors in SMEM (else in the instance's HBM block)
   int32_t fuse_min;                // local FFT length from which radix-16 passes are used
+  int32_t chunk;                   // column pairs per chunk of the unstaged column stage
   double tol;
   double scale_e, scale_p;         // 1/(4L) folding of the real-FFT split and 1/L
   double qscale_p;                 // Lambda_Q scale of the preconditioner: 1 or (n-1)/n
@@ -64,6 +65,7 @@ struct Plan {
   int32_t staged = 0;   // cross-CTA step staged through SMEM buffers B (staging) and O (output)
   int32_t resident = 0; // per-instance constant tables cached in SMEM (small local length)
   int32_t fuse_min = 1024;   // radix-16 passes from L1 = 1024 (measured, tools/fft_ubench.cu)
+  int32_t chunk = 0;         // unstaged clusters: column pairs per chunk (chunk buffer 2 chunk C complex)
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
@@ -131,11 +133,13 @@ DevParams dev_params(const Plan &pl, char *ws);
 // [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], per-level multipliers
 // [L1e + L1p], pair twiddles [L1e + L1p] (double2), Krylov vectors [kSmemVec x L1p] (double2) if
 // vsmem; 48 doubles of reduction scratch, 128 doubles of pushed CTA partials and 4 mbarriers.
-TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem) {
+TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem,
+                                 int64_t chunk_cplx = 0) {
   int64_t c2 = (staged ? 3 * L1e : L1e) + (staged ? 2 : 1) * kPadBuf * (L1e / 16);   // A (+ B, O)
   if (resident) c2 += L1e + 3 * (L1e + L1p);      // twiddles, column twiddles, multipliers, pair twiddles
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;
+  if (!staged) c2 += chunk_cplx;                   // chunk buffer of the unstaged column stage
   int64_t d = 48 + 128 + 4;                        // reductions, push buffers, mbarriers
   return 16 * c2 + 8 * d + 64;
 }

@@ -24,6 +24,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tsf_plan.h"
 
 namespace cg = cooperative_groups;
@@ -150,6 +152,15 @@ __device__ __forceinline__ void push1(uint32_t dst, double v, uint32_t mb) {
                "r"(mb)
                : "memory");
 }
+__device__ __forceinline__ int64_t ld_acquire(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int64_t *p, int64_t v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Exchange state of one CTA: counts of operator exchanges and reductions so far (identical in
 // every thread of the cluster, since control flow is uniform); they select mbarrier phases.
 struct Xch {
@@ -1181,7 +1192,7 @@ struct T5 { double2 a, b, c, d, f; };
 template <int C, bool STG>
 __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
                                             const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
-                                            double2 *Hsum, Xch &xs) {
+                                            double2 *Hsum, Xch &xs, bool use_pre = false) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
@@ -1192,8 +1203,22 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
   // the RHS anyway): two elements per thread and HU rows per batch, all loads of a batch issued
   // before the FMAs (HU x 2 loads in flight per thread; the sum streams j rows of the CTA chunk)
   double2 *Hs = Hsum;
-  if (j >= 1) {
+  if (use_pre) {
+    // history pre-sum P^j = kappa (e_j d^0 + sum_{s=1}^{j-2} chat_{j-s} d^s) from the helper CTAs
+    // (computed during level j-1); add the newest row kappa chat_1 d^{j-1}
+    if (threadIdx.x == 0) {
+      while (ld_acquire(P.sync + 1 + (j & 1)) != j) __nanosleep(64);
+    }
+    __syncthreads();
+    const double2 *Pj = reinterpret_cast<const double2 *>(P.pre) + (j & 1) * hstride + r * npc;
+    const double w1 = I.hwc[1];
+    TSF_FOR_E(npc) { Hs[e] = caxpy(w1, H[(j - 1) * hstride + e], __ldcg(Pj + e)); }
+  } else if (j >= 1) {
+    // the same summation order as the helpers (P^j over rows 1..j-2 with HU-row batches and two
+    // accumulators, then + chat_1 d^{j-1}), so step-wise and helper-assisted runs agree bitwise;
+    // two elements per thread, all loads of a batch issued before the FMAs
     constexpr int HU = C == 1 ? 4 : 8;
+    const double w1 = I.hwc[1];
     for (int e0 = threadIdx.x; e0 < npc; e0 += 2 * kThreads) {
       const int e1 = e0 + kThreads;
       const bool has1 = e1 < npc;
@@ -1201,7 +1226,7 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
       double2 a0 = cscale(H[e0], wj), a1 = has1 ? cscale(H[e1], wj) : zero2();
       double2 b0 = zero2(), b1 = zero2();
       int64_t s = 1;
-      for (; s + HU - 1 <= j - 1; s += HU) {
+      for (; s + HU - 1 <= j - 2; s += HU) {
         double2 v0[HU], v1[HU];
         double w[HU];
 #pragma unroll
@@ -1218,13 +1243,18 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
           b1 = caxpy(w[u + 1], v1[u + 1], b1);
         }
       }
-      for (; s <= j - 1; ++s) {
+      for (; s <= j - 2; ++s) {
         const double w = I.hwc[j - s];
         a0 = caxpy(w, H[s * hstride + e0], a0);
         if (has1) a1 = caxpy(w, H[s * hstride + e1], a1);
       }
-      Hs[e0] = cadd(a0, b0);
-      if (has1) Hs[e1] = cadd(a1, b1);
+      if (j >= 2) {
+        Hs[e0] = caxpy(w1, H[(j - 1) * hstride + e0], cadd(a0, b0));
+        if (has1) Hs[e1] = caxpy(w1, H[(j - 1) * hstride + e1], cadd(a1, b1));
+      } else {
+        Hs[e0] = a0;
+        if (has1) Hs[e1] = a1;
+      }
     }
   }
   TSF_PACC(sm, PS_RHS_HIST);
@@ -1329,6 +1359,10 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
     I.st[j] = isfinite(relres) ? TSF_LEVEL_OK : TSF_LEVEL_DIVERGED;
   }
   __syncthreads();
+  if (P.helpers > 0 && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(reinterpret_cast<unsigned long long *>(P.sync), 1ull);
+  }
 }
 
 // Views (carve-up, instance, vectors) are computed by every thread from the kernel's own
@@ -1339,7 +1373,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
 // history or statistics.
 template <int C, int METHOD, bool STG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
-                                            int64_t j, uint32_t r, Xch &xs, int mode = 0) {
+                                            int64_t j, uint32_t r, Xch &xs, int mode = 0, int64_t j0 = 0) {
   const int npc = P.L1p;
   const int64_t n = P.n;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
@@ -1357,7 +1391,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 
   double g2[1] = {0.0};
   if (mode == 0) {
-    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, V.X, xs);
+    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, V.X, xs, P.helpers > 0 && j >= 2 && j >= j0 + 1);
   } else {
     // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
     const int64_t m = mode == 1 ? 0 : n / 2 - 1;
@@ -1648,6 +1682,10 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     I.st[j] = status;
   }
   __syncthreads();
+  if (P.helpers > 0 && threadIdx.x == 0) {   // this CTA's slice of d^j is written
+    __threadfence();
+    atomicAdd(reinterpret_cast<unsigned long long *>(P.sync), 1ull);
+  }
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     sm.prof[PS_LEVEL] += (unsigned long long)(clock64() - tlev0);
@@ -1656,11 +1694,71 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 #endif
 }
 
+// ------------------------------------------------------------------------ history helpers
+// Single-instance solves occupy one cluster (C3: 16 of 148 SMs).  Extra clusters of the same
+// launch ("helpers", all co-resident: the launcher checks cudaOccupancyMaxActiveClusters) stream
+// the history while the solver iterates: during level J-1 they form the pre-sum
+//   P^J = kappa (e_J d^0 + sum_{s=1}^{J-2} chat_{J-s} d^s)
+// (eq3.1's memory term without its newest row) into pre[J & 1]; the solver then needs only
+// kappa chat_1 d^{J-1}.  Protocol: solver CTAs count finished levels in sync[0] (release by
+// fence + atomic); helpers wait for C (J - 1 - j0) of them, write their slice, count themselves
+// in sync[3 + (J & 1)], and the last one publishes ready[J & 1] = J (release store).
+template <int C>
+__device__ void hist_helper(const DevParams &P, int32_t nlev) {
+  const Inst I = inst_view(P, 0);
+  const int h = int(blockIdx.x) - P.B * C, nh = P.helpers;
+  const int64_t n = P.n, half = n / 2;
+  const int64_t j0 = *P.level, jend = (j0 + nlev < P.M) ? j0 + nlev : P.M;
+  const double2 *Hd = reinterpret_cast<const double2 *>(I.hist);
+  for (int64_t J = (j0 + 1 > 2 ? j0 + 1 : 2); J < jend; ++J) {
+    if (threadIdx.x == 0) {
+      while (ld_acquire(P.sync) < int64_t(C) * (J - 1 - j0)) __nanosleep(256);
+    }
+    __syncthreads();
+    double2 *Pj = reinterpret_cast<double2 *>(P.pre) + (J & 1) * half;
+    const double wJ = I.hwe[J];
+    for (int64_t e = int64_t(h) * kThreads + threadIdx.x; e < half; e += int64_t(nh) * kThreads) {
+      double2 a = cscale(__ldcg(Hd + e), wJ), b = zero2();
+      int64_t s = 1;
+      for (; s + 7 <= J - 2; s += 8) {
+        double2 v[8];
+        double w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = __ldcg(Hd + (s + u) * half + e);
+          w[u] = I.hwc[J - s - u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          a = caxpy(w[u], v[u], a);
+          b = caxpy(w[u + 1], v[u + 1], b);
+        }
+      }
+      for (; s <= J - 2; ++s) a = caxpy(I.hwc[J - s], __ldcg(Hd + s * half + e), a);
+      Pj[e] = cadd(a, b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long *cnt = reinterpret_cast<unsigned long long *>(P.sync + 3 + (J & 1));
+      if (atomicAdd(cnt, 1ull) == (unsigned long long)(nh - 1)) {
+        *cnt = 0ull;
+        __threadfence();
+        st_release(P.sync + 1 + (J & 1), J);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------ kernels
 template <int C, int METHOD, bool STG, bool VS>
 __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
     k_solve(DevParams P, int32_t nlev, int32_t mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (int(blockIdx.x) >= P.B * C) {   // history-helper clusters (single-instance launches)
+    if constexpr (C > 1) hist_helper<C>(P, nlev);
+    return;
+  }
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
@@ -1686,7 +1784,7 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   if (mode != 0) {               // NEXT-2 setup solve with the level-1 operators
     level_solve<C, METHOD, STG>(P, I, sm, V, 1, r, xs, mode);
   } else {
-    for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs);
+    for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs, 0, j0);
   }
   if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
 #ifdef TSF_PROFILE
@@ -1806,6 +1904,52 @@ cudaError_t launch_cluster(K kern, const Plan &pl, int grid, cudaStream_t st, Ar
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Launch of a solve kernel, with history-helper clusters for multi-level single-instance
+// cluster solves when the GPU can keep them all resident at once (they spin on each other).
+template <class K>
+cudaError_t launch_solve_k(K kern, const Plan &pl, const DevParams &dp0, int32_t nlev, cudaStream_t st,
+                           int32_t mode) {
+  DevParams dp = dp0;
+  dp.helpers = 0;
+  int grid = pl.B * pl.C;
+  if (pl.B == 1 && pl.C > 1 && nlev >= 3 && mode == 0 && std::getenv("TSF_NO_HELPERS") == nullptr) {
+    const int64_t cta_need = (pl.n / 2 + kThreads - 1) / kThreads;
+    int hcl = int((cta_need + pl.C - 1) / pl.C);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+    if (e != cudaSuccess) return e;
+    if (pl.C > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((1 + hcl) * pl.C));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = size_t(pl.smem);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(pl.C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess) {
+      if (hcl > active - 1) hcl = active - 1;
+      if (hcl > 0) {
+        dp.helpers = hcl * pl.C;
+        grid = (1 + hcl) * pl.C;
+        e = cudaMemsetAsync(dp.sync, 0, 8, st);                 // solver CTA-levels done
+        if (e == cudaSuccess) e = cudaMemsetAsync(dp.sync + 1, 0xff, 16, st);   // ready[] = -1
+        if (e == cudaSuccess) e = cudaMemsetAsync(dp.sync + 3, 0, 16, st);      // counters
+        if (e != cudaSuccess) return e;
+      }
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  return launch_cluster(kern, pl, grid, st, dp, nlev, mode);
+}
+
 // Staged exchange (STG) exists for C > 1 only.
 #define TSF_STG_OF(CC, pl) ((CC) > 1 && (pl).staged)
 // Solve-kernel launchers per (cluster size, method), each instantiated in its own translation unit
@@ -1816,13 +1960,12 @@ cudaError_t launch_solve_cm(const Plan &pl, const DevParams &dp, int32_t nlev, c
   template <>                                                                                   \
   cudaError_t launch_solve_cm<CC, MM>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, \
                                       int32_t z) {                                              \
-    const int g = pl.B * CC;                                                                    \
     constexpr bool S1 = (CC) > 1;                                                               \
     const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
-    if (stg && vs) return launch_cluster(k_solve<CC, MM, S1, true>, pl, g, st, dp, nlev, z);    \
-    if (stg) return launch_cluster(k_solve<CC, MM, S1, false>, pl, g, st, dp, nlev, z);         \
-    if (vs && CC == 1) return launch_cluster(k_solve<CC, MM, false, CC == 1>, pl, g, st, dp, nlev, z); \
-    return launch_cluster(k_solve<CC, MM, false, false>, pl, g, st, dp, nlev, z);               \
+    if (stg && vs) return launch_solve_k(k_solve<CC, MM, S1, true>, pl, dp, nlev, st, z);       \
+    if (stg) return launch_solve_k(k_solve<CC, MM, S1, false>, pl, dp, nlev, st, z);            \
+    if (vs && CC == 1) return launch_solve_k(k_solve<CC, MM, false, CC == 1>, pl, dp, nlev, st, z); \
+    return launch_solve_k(k_solve<CC, MM, false, false>, pl, dp, nlev, st, z);                  \
   }
 #define TSF_INSTANTIATE_CLUSTER(CC)                                                             \
   template <>                                                                                   \

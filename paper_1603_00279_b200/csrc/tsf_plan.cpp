@@ -191,6 +191,8 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.off_sq_e = o;    o = up(o + size_t(n) * 8);
   P.off_sq_p = o;    o = up(o + size_t(n / 2) * 8);
   P.off_level = o;   o = up(o + 64);
+  P.off_sync = o;    o = up(o + 64);
+  P.off_pre = o;     o = up(o + (B == 1 ? size_t(2) * size_t(n) * 8 : 0));
   P.off_prof = o;    o = up(o + 32 * 8);
   // init scratch (batched spectra FFTs): per instance 2 x (2n + n) complex
   const size_t per = size_t(3 * n) * 16 * 2;
@@ -328,6 +330,9 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.sq_e = reinterpret_cast<const double *>(ws + pl.off_sq_e);
   d.sq_p = reinterpret_cast<const double *>(ws + pl.off_sq_p);
   d.level = reinterpret_cast<int64_t *>(ws + pl.off_level);
+  d.sync = reinterpret_cast<int64_t *>(ws + pl.off_sync);
+  d.pre = reinterpret_cast<double *>(ws + pl.off_pre);
+  d.helpers = 0;
   d.prof = reinterpret_cast<unsigned long long *>(ws + pl.off_prof);
   d.inst = ws + pl.off_inst;
   d.stride = int64_t(pl.stride);

@@ -47,6 +47,9 @@ struct DevParams {
   const int32_t *slot_e, *slot_p;  // k1 -> slot of the local DIF output
   const double *sq_e, *sq_p;       // sin tables in task order
   int64_t *level;                  // device level counter
+  int64_t *sync;                   // history helpers: [0] solver CTA-levels done, [1..2] ready[J&1], [3] counters
+  double *pre;                     // history pre-sums P^J, two n-vectors (J & 1), single-instance plans
+  int32_t helpers;                 // history-helper CTAs of this launch (0: the solver sums the history)
   unsigned long long *prof;        // 32 cycle counters (profiling build only)
   // per-instance block
   char *inst;                      // base of instance 0
@@ -70,6 +73,7 @@ struct Plan {
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
   size_t off_level = 0, off_prof = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
+  size_t off_sync = 0, off_pre = 0;
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;

@@ -874,6 +874,21 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   TSF_PACC(sm, PS_BAR3);
 }
 
+// Column twiddles W^{q k1}, q < C, from the single table value w = W^{k1}: products in a binary
+// tree (depth log2 C), so each power carries at most log2(C) rounding steps; one global load
+// per column instead of C - 1.
+template <int C>
+__device__ __forceinline__ void col_twiddles(double2 w, double2 (&wq)[C]) {
+  wq[0] = make_double2(1.0, 0.0);
+  if constexpr (C > 1) wq[1] = w;
+#pragma unroll
+  for (int p = 2; p < C; p *= 2) {
+    wq[p] = cmul(wq[p / 2], wq[p / 2]);
+#pragma unroll
+    for (int q = 1; q < p && p + q < C; ++q) wq[p + q] = cmul(wq[p], wq[q]);
+  }
+}
+
 // C > 1 without room for B and O (L1 = 8192, C5): the column stage in chunks of CP column
 // pairs through a chunk buffer Bc (layout Bc[q * 2CP + 2 il + ab], conflict-free column reads).
 // Per chunk: pull the rows of its columns from every CTA's A (DSMEM), column DFT_C, bin pairs,
@@ -883,7 +898,8 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
 // push before the local inverse FFTs.
 template <int C>
 __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, const Geo &g, const SpecOp &op,
-                                              const double2 *__restrict__ tw, uint32_t r) {
+                                              const double2 *__restrict__ tw, uint32_t r, const Smem &sm) {
+  TSF_PT0();
   const int L1 = g.L1, np = g.np, l1 = g.l1;
   const int W = 2 * CP;                       // columns per chunk
   for (int c0 = 0; c0 < np; c0 += CP) {
@@ -895,18 +911,22 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
       Bc[q * W + col] = remote<C>(A, uint32_t(q))[pidx(dslot(k1, l1))];
     }
     __syncthreads();
+    TSF_PACC(sm, PS_GATHER);
     for (int col = threadIdx.x; col < 2 * cp; col += kThreads) {   // column DFT_C
       const int k1 = col_k1(L1, C, r, 2 * c0 + col);
       double2 z[C];
 #pragma unroll
       for (int q = 0; q < C; ++q) z[q] = Bc[q * W + col];
+      double2 wq[C];
+      col_twiddles<C>(tw[k1 * g.twL], wq);
 #pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], wq[q]);
       fft_reg<C, false>(z);
 #pragma unroll
       for (int q = 0; q < C; ++q) Bc[q * W + col] = z[q];
     }
     __syncthreads();
+    TSF_PACC(sm, PS_COLF);
     // bin pairs: item u = k2 * cp + il; (row k2, col (il,0)) <-> (row C-1-k2, col (il,1))
     for (int u = threadIdx.x; u < C * cp; u += kThreads) {
       const int k2 = u / cp, il = u - k2 * cp, i = c0 + il;
@@ -960,19 +980,23 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
       }
     }
     __syncthreads();
+    TSF_PACC(sm, PS_PAIRS);
     for (int col = threadIdx.x; col < 2 * cp; col += kThreads) {   // inverse column DFT_C + push
       const int k1 = col_k1(L1, C, r, 2 * c0 + col);
       double2 z[C];
 #pragma unroll
       for (int q = 0; q < C; ++q) z[q] = Bc[q * W + col];
       fft_reg<C, true>(z);
+      double2 wq[C];
+      col_twiddles<C>(tw[k1 * g.twL], wq);
 #pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], wq[q]);
       const int s = pidx(dslot(k1, l1));
 #pragma unroll
       for (int q = 0; q < C; ++q) remote<C>(A, uint32_t(q))[s] = z[q];
     }
     __syncthreads();                            // Bc is refilled by the next chunk
+    TSF_PACC(sm, PS_COLI);
   }
 }
 
@@ -1004,7 +1028,7 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
     } else {
       csync<C>();                // every local transform done before remote gathers
       TSF_PACC(sm, PS_BAR1);
-      cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r);
+      cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r, sm);
       csync<C>();                // every push landed before the local inverse transforms
       TSF_PACC(sm, PS_BAR3);
     }

@@ -257,6 +257,50 @@ def test_step_graph_equals_one_shot_solve_and_is_deterministic():
     np.testing.assert_array_equal(it1, s.stats()[0])
 
 
+@pytest.mark.parametrize("method,cluster", [("bicgstab", 16), ("bicgstab", 2), ("gsf", 16), ("pcgs", 4)])
+def test_history_helper_clusters_match_the_solver_own_history_bitwise(method, cluster, monkeypatch):
+    """Single-instance solves launch helper clusters that stream the history pre-sums during the
+    previous level (DESIGN.md \"History pre-sums\"); the result must equal the helper-free run
+    bit for bit (same summation order), and the oracle within the parity bar."""
+    f = np.random.default_rng(5).standard_normal((24, 1024))
+    inst, p = pair(0.7, 1.6, 1024, 24, gamma=(O.CONST, 0.8), dplus=(O.CONST, 1.5), dminus=(O.CONST, 0.4),
+                   src="table", f_table=f)
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("TSF_NO_HELPERS", "1")
+        s = tsf.Solver([inst], method=method, cluster=cluster)
+        s.solve()
+        assert s.sync() >= 0
+        outs.append((s.solution(0), s.stats()[0].copy()))
+        s.close()
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    Uo = O.solve(p)
+    assert np.linalg.norm(outs[0][0] - Uo[-1]) <= RTOL * np.linalg.norm(Uo[-1])
+
+
+def test_next4_spectrum_export_matches_oracle_and_clusters_at_one(tmp_path):
+    """NEXT-4 (Figs. fig1/fig2): the dense level matrix assembled from the GPU operator
+    equals the oracle's, and the Strang-preconditioned spectrum is clustered at 1 with "about
+    6~10" outliers at most and no eigenvalue near 0.  Example 1 coefficients
+    (P:931-944: d+ = 0.8, d- = 0.5, gamma = -0.1), alpha = 0.9, beta = 1.8, N = M = 128."""
+    import os
+    from paper_1603_00279_b200 import spectra_export as X
+    inst, p = pair(0.9, 1.8, 128, 4, gamma=(O.CONST, -0.1), dplus=(O.CONST, 0.8), dminus=(O.CONST, 0.5),
+                   src="zero")
+    s = tsf.Solver([inst])
+    for j in (0, 1):
+        A = X.dense_operator(s, j)
+        Ao, _ = O.assemble(p, j)
+        assert np.abs(A - Ao).max() <= 1e-12 * np.abs(Ao).max()
+        _, ep = X.level_spectra(s, j)
+        summ = X.cluster_summary(ep, 1.0, 0.1)
+        assert summ["outliers"] <= 10 and summ["min_real"] > 0.1, summ
+    files = X.export_csv(str(tmp_path), s)
+    assert len(files) == 2 and all(os.path.getsize(f) > 1000 for f in files)
+
+
 def test_zero_operator_and_stability_invariants():
     # gamma = d = 0, f = 0: u^j = phi for all j (S:396); f = 0 -> ||u^j|| <= ||u^0|| (S:413)
     inst = Instance(0.4, 1.5, 128, 6, const(0.0), const(0.0), const(0.0), "zero")

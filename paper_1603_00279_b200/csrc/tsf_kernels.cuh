@@ -195,13 +195,16 @@ struct Smem {
 // Section timers (profiling build, -DTSF_PROFILE): thread 0 of block 0 accumulates clock64
 // cycles per section into P.prof[slot]; the wait at a barrier is charged to the section
 // that ends with it.
+#ifndef TSF_PROF_CTA
+#define TSF_PROF_CTA 0   // the CTA whose section times are recorded (profiling build)
+#endif
 #ifdef TSF_PROFILE
 #define TSF_PT0() long long tsf_pt_ = clock64()
 #define TSF_PTR() tsf_pt_ = clock64()
 #define TSF_PACC(sm, slot)                                                                    \
   do {                                                                                      \
     const long long t_ = clock64();                                                         \
-    if (threadIdx.x == 0 && blockIdx.x == 0) (sm).prof[slot] += (unsigned long long)(t_ - tsf_pt_); \
+    if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) (sm).prof[slot] += (unsigned long long)(t_ - tsf_pt_); \
     tsf_pt_ = t_;                                                                           \
   } while (0)
 #else
@@ -632,6 +635,7 @@ struct SpecOp {
                         // from lam/sq on the fly (the once-per-level B operator)
   const double2 *pw;    // resident: pair twiddles W_{2L}^{bin} of this CTA's slice, else nullptr
   double2 nyq;          // base spectrum at the Nyquist bin L
+  double2 nyqe;         // effective multiplier at the Nyquist bin (formed once by make_op)
   int np;               // column-pair tasks per CTA
   int rC;               // r * C: task-order index base of this CTA in the global tables
   bool mul_sh;          // mul is this CTA's slice in SMEM (else the global task-order table)
@@ -716,7 +720,7 @@ __device__ __forceinline__ void pointwise_local(double2 *A, const Geo &g, const 
     if (i == 0) {
       const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
       double2 a = A[sa], b = A[sb];
-      pair_self(a, op.get(0, 0, 0, 0), op.nyquist(g.L), tw[0], op.scale);
+      pair_self(a, op.get(0, 0, 0, 0), op.nyqe, tw[0], op.scale);
       const double2 lm = op.get(0, 1, 0, g.L / 2);
       pair_self(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
       A[sa] = a; A[sb] = b;
@@ -791,59 +795,44 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   }
   __syncthreads();
   TSF_PACC(sm, PS_COLF);
-  // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1))
+  // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1)).
+  // The pseudo column pair (0, L1/2) of CTA 0 is done afterwards by warp 0, one pair per lane:
+  // inside the item loop its branch diverged from the regular lanes in every warp and made
+  // CTA 0's stage ~2.4x longer than its peers' (measured), which all of them then waited for.
   for (int u = threadIdx.x; u < np * C; u += kThreads) {
     const int k2 = u >> g.lnp, i = u & (np - 1);
     const int pi = int(r) + i * C;
-    if (pi != 0) {
-      const int bin = pi + L1 * k2;
-      double2 &za = B[k2 * ncol + i];
-      double2 &zb = B[(C - 1 - k2) * ncol + np + i];
-      double2 a = za, b = zb;
-      pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
-                 op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
-      za = a;
-      zb = b;
-    } else {
-      // column 0 (bins L1 k2) pairs k2 <-> (C - k2) mod C; k2 = 0 pairs with the Nyquist bin
-      const int kk = (C - k2) % C;
-      if (k2 <= C / 2) {
-        const int bin = L1 * k2;
-        const double2 la = op.get(k2, 0, 0, bin);
-        const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
-        double2 &za = B[k2 * ncol];
-        if (kk == k2) {
-          double2 a = za;
-          pair_self(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
-          za = a;
-        } else {
-          double2 &zb = B[kk * ncol];
-          double2 a = za, b = zb;
-          pair_apply(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
-          za = a;
-          zb = b;
-        }
-      }
-      // column L1/2 (bins L1/2 + L1 k2) pairs k2 <-> C-1-k2
-      const int km = C - 1 - k2;
-      if (k2 < (C + 1) / 2) {
-        const int bin = L1 / 2 + L1 * k2;
-        const double2 la = op.get(k2, 1, 0, bin);
-        const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
-        double2 &za = B[k2 * ncol + np];
-        if (km == k2) {
-          double2 a = za;
-          pair_self(a, la, la, w, op.scale);
-          za = a;
-        } else {
-          double2 &zb = B[km * ncol + np];
-          double2 a = za, b = zb;
-          pair_apply(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
-          za = a;
-          zb = b;
-        }
-      }
-    }
+    if (pi == 0) continue;
+    const int bin = pi + L1 * k2;
+    double2 &za = B[k2 * ncol + i];
+    double2 &zb = B[(C - 1 - k2) * ncol + np + i];
+    double2 a = za, b = zb;
+    pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
+               op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
+    za = a;
+    zb = b;
+  }
+  if (r == 0 && threadIdx.x < C / 2 + 1 + (C + 1) / 2) {
+    // one bin pair per lane, branch-free (operands selected, a single pair_apply):
+    // column 0 (bins L1 k2): k2 <-> (C - k2) mod C, k2 = 0 with the Nyquist bin;
+    // column L1/2 (bins L1/2 + L1 k2): k2 <-> C - 1 - k2
+    const int o = threadIdx.x;
+    const bool c0 = o <= C / 2;
+    const int k2 = c0 ? o : o - (C / 2 + 1);
+    const int kp = c0 ? (C - k2) % C : C - 1 - k2;
+    const int ab = c0 ? 0 : 1;
+    const int cof = c0 ? 0 : np;
+    const int bin = c0 ? L1 * k2 : L1 / 2 + L1 * k2;
+    const bool self = kp == k2;
+    const double2 la = op.get(k2, ab, 0, bin);
+    const double2 lp = op.get(kp, ab, 0, g.L - bin);
+    const double2 lb = self ? ((c0 && k2 == 0) ? op.nyqe : la) : lp;
+    const double2 w = op.wtw(k2, ab, 0, bin, tw, g.tw2L);
+    double2 &za = B[k2 * ncol + cof];
+    double2 a = za, b = self ? za : B[kp * ncol + cof];
+    pair_apply(a, b, la, lb, w, op.scale);
+    za = a;
+    if (!self) B[kp * ncol + cof] = b;
   }
   __syncthreads();
   TSF_PACC(sm, PS_PAIRS);
@@ -949,7 +938,7 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
           double2 &za = Bc[k2 * W];
           if (kk == k2) {
             double2 a = za;
-            pair_self(a, la, k2 == 0 ? op.nyquist(g.L) : la, w, op.scale);
+            pair_self(a, la, k2 == 0 ? op.nyqe : la, w, op.scale);
             za = a;
           } else {
             double2 &zb = Bc[kk * W];
@@ -1037,7 +1026,7 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
   local_fft<true>(Y, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
-  if (threadIdx.x == 0 && blockIdx.x == 0) sm.prof[PS_APPLIES] += 1;
+  if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
 #endif
   return Y;
 }
@@ -1104,6 +1093,7 @@ __device__ __forceinline__ SpecOp make_op(const DevParams &P, const Inst &I, int
     op.conj = (which == OP_PTINV);
     op.div = true;
   }
+  op.nyqe = op.nyquist(which <= OP_AT ? int(P.n) : int(P.n / 2));
   return op;
 }
 
@@ -1153,6 +1143,7 @@ __device__ __forceinline__ SpecOp make_gsf_op(const DevParams &P, const Inst &I,
   op.scale = P.scale_e;
   op.conj = false;
   op.div = false;
+  op.nyqe = op.nyq;
   return op;
 }
 
@@ -1813,7 +1804,7 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
 #ifdef TSF_PROFILE
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
+  if (blockIdx.x == TSF_PROF_CTA && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
 #endif
   csync<C>();                    // no CTA leaves while a peer may still push into it
 }
@@ -1865,7 +1856,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
 #ifdef TSF_PROFILE
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
+  if (blockIdx.x == TSF_PROF_CTA && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
 #endif
   csync<C>();
 }

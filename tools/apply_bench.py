@@ -21,7 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=400)
 ap.add_argument("--cases", default="C3:16,C3:8,C2:2,C4:1,C5:16")
 a = ap.parse_args()
-prof = os.environ.get("TSF_LIB_VARIANT") == "prof"
+prof = os.environ.get("TSF_LIB_VARIANT", "").startswith("prof")
 for case in a.cases.split(","):
     cfg, cl = case.split(":")
     inst = CONFIGS[cfg]()[0]

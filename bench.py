@@ -187,6 +187,14 @@ def oracle_rate(cfg):
     return M / full, sample, full * B
 
 
+def base_config(args):
+    """Workload keys shared by both arms (the GPU arm adds its launch shape)."""
+    from paper_1603_00279_b200.inputs import CONFIGS
+    insts = CONFIGS[args.config]()
+    return {"workload": args.config, "n": insts[0].n, "M": insts[0].M, "instances": len(insts),
+            "method": args.method, "precond": args.precond, "tol": 1e-12}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -204,7 +212,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * statistics.mean(t for _, t in vals), "higher_is_better": True,
             "scaling": "weak" if args.config in ("C1", "C2", "C3") else "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": {"workload": args.config},
+            "dtype": "f64", "data": "synthetic", "config": base_config(args),
             "cpu_baseline": {"value": value, "unit": "levels/s", "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "levels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -347,9 +355,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step_ms,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.config, "n": n, "M": M, "instances": units_total,
-                       "method": args.method, "precond": args.precond, "cluster": info.cluster,
-                       "l2": "flushed between steps (512 MiB write)", "tol": 1e-12},
+            "config": {**base_config(args), "instances": units_total, "cluster": info.cluster,
+                       "l2": "flushed between steps (512 MiB write)"},
             "krylov_iters_per_s": iters_per_s,
             "mean_iters_per_level": iters_job / levels_job,
             "init_s": t_init,

@@ -32,3 +32,6 @@ for c in C2 C4 C5; do
 done
 python tools/ncu_keys.py $O/c3_full_raw.csv > $O/c3_full_keys.txt 2>&1
 python tools/ncu_summary.py launches $O/launches.csv > $O/launches_summary.txt 2>&1
+timeout 600 python bench.py --config C3 --method gsf --steps 3 --warmup 3 --no-e2e --no-cpu > $O/bench_C3_gsf.json 2>&1
+timeout 600 python bench.py --config C3 --method pcgs --steps 3 --warmup 3 --no-e2e --no-cpu > $O/bench_C3_pcgs.json 2>&1
+TSF_LIB_VARIANT=prof timeout 300 python tools/apply_bench.py > $O/apply_bench_prof.txt 2>&1

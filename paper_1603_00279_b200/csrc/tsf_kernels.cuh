@@ -1535,67 +1535,66 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     // Preconditioned CGS (the paper's PCGS; MATLAB pcgs), right-preconditioned:
     // shadow rt = r0, u = r + beta q, p = u + beta (q + beta p), phat = P^{-1} p, vhat = A phat,
     // alpha = rho / (rt.vhat), q = u - alpha vhat, uhat = P^{-1}(u + q), x += alpha uhat,
-    // r -= alpha A uhat.  Vector slots: u -> S, p -> PV, q -> VV, phat -> PH, uhat -> SH.
-    double rho = rr0, rho_prev = 1.0;
-    for (int it = 0;; ++it) {
-      const double beta = it == 0 ? 0.0 : rho / rho_prev;
-      if (it == 0) {
-        TSF_FOR_E(npc) {
-          const double2 rv = R[e];
-          S[e] = rv;
-          PV[e] = rv;
-          sm.A[pidx(e)] = rv;
-        }
+    // r -= alpha A uhat.  Vector slots: u -> S, p -> PV, q -> VV, phat -> PH.  As for BiCGSTAB,
+    // the four applications of an iteration (h = 0..3: P^{-1}, A, P^{-1}, A) share one inlined
+    // apply.
+    double rho = rr0, alpha = 0.0;
+    TSF_FOR_E(npc) {                           // u_0 = p_0 = r_0
+      const double2 rv = R[e];
+      S[e] = rv;
+      PV[e] = rv;
+      sm.A[pidx(e)] = rv;
+    }
+    for (int h = 0;; h = (h + 1) & 3) {
+      const bool isP = !(h & 1);
+      if (isP && !prec) {
+        Y = sm.A;
       } else {
-        batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
-                               [&](int e, T3 &t) {
-                                 const double2 u = caxpy(beta, t.b, t.a);
-                                 const double2 pv = caxpy(beta, caxpy(beta, t.c, t.b), u);
-                                 S[e] = u;
-                                 PV[e] = pv;
-                                 sm.A[pidx(e)] = pv;
-                               });
+        __syncthreads();
+        const SpecOp op = isP ? opP : opA;
+        const Geo g = isP ? gp : ge;
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
       }
-      __syncthreads();
-      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
-      TSF_FOR_E(npc) {
-        const double2 ph = Y[pidx(e)];
-        PH[e] = ph;
-        sm.A[pidx(e)] = ph;
-        sm.A[pidx(e + npc)] = zero2();
+      if (h == 0) {                            // phat
+        TSF_FOR_E(npc) {
+          const double2 ph = Y[pidx(e)];
+          PH[e] = ph;
+          sm.A[pidx(e)] = ph;
+          sm.A[pidx(e + npc)] = zero2();
+        }
+        continue;
       }
-      __syncthreads();
-      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
-      double sg[1] = {0.0};
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; },
-                             [&](int e, T1 &t) { sg[0] += cdot(t.a, Y[pidx(e)]); });
-      csum<C, 1>(sg, sm, xs);
-      if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      const double alpha = rho / sg[0];
-      // q = u - alpha vhat, then P^{-1}(u + q); the apply output Y still holds vhat (when Y is
-      // A itself each thread reads its element before overwriting it)
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = S[e]; }, [&](int e, T1 &t) {
-        const double2 q = caxpy(-alpha, Y[pidx(e)], t.a);
-        VV[e] = q;
-        sm.A[pidx(e)] = cadd(t.a, q);
-      });
-      __syncthreads();
-      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = X[e]; }, [&](int e, T1 &t) {
-        const double2 uh = Y[pidx(e)];
-        X[e] = caxpy(alpha, uh, t.a);
-        sm.A[pidx(e)] = uh;
-        sm.A[pidx(e + npc)] = zero2();
-      });
-      __syncthreads();
-      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+      if (h == 1) {                            // vhat: alpha, q = u - alpha vhat, A <- u + q
+        double sg[1] = {0.0};
+        TSF_FOR_E(npc) { sg[0] += cdot(RH[e], Y[pidx(e)]); }
+        csum<C, 1>(sg, sm, xs);
+        if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        alpha = rho / sg[0];
+        TSF_FOR_E(npc) {                       // Y may alias A: read before the write
+          const double2 u = S[e];
+          const double2 q = caxpy(-alpha, Y[pidx(e)], u);
+          VV[e] = q;
+          sm.A[pidx(e)] = cadd(u, q);
+        }
+        continue;
+      }
+      if (h == 2) {                            // uhat: x += alpha uhat, A <- uhat
+        TSF_FOR_E(npc) {
+          const double2 uh = Y[pidx(e)];
+          X[e] = caxpy(alpha, uh, X[e]);
+          sm.A[pidx(e)] = uh;
+          sm.A[pidx(e + npc)] = zero2();
+        }
+        continue;
+      }
+      // h == 3: A uhat: r -= alpha A uhat; rho' = rt.r; ||r||
       double rr[2] = {0.0, 0.0};
-      batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = R[e]; t.b = RH[e]; }, [&](int e, T2 &t) {
-        const double2 rn = caxpy(-alpha, Y[pidx(e)], t.a);
+      TSF_FOR_E(npc) {
+        const double2 rn = caxpy(-alpha, Y[pidx(e)], R[e]);
         R[e] = rn;
-        rr[0] += cdot(t.b, rn);
+        rr[0] += cdot(RH[e], rn);
         rr[1] += cdot(rn, rn);
-      });
+      }
       csum<C, 2>(rr, sm, xs);
       hs += 2;
       relres = sqrt(rr[1]) / rn0;
@@ -1603,79 +1602,91 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       if (relres < P.tol) break;
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
       if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      rho_prev = rho;
+      const double beta = rr[0] / rho;
       rho = rr[0];
+      TSF_FOR_E(npc) {                         // u = r + beta q; p = u + beta (q + beta p)
+        const double2 q = VV[e];
+        const double2 u = caxpy(beta, q, R[e]);
+        const double2 pv = caxpy(beta, caxpy(beta, PV[e], q), u);
+        S[e] = u;
+        PV[e] = pv;
+        sm.A[pidx(e)] = pv;
+      }
     }
   } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
-    // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r, p = z.
+    // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r = P^{-T} A^T r, p = z;
+    // per iteration phat = P^{-1} p, q = A phat, a = gamma/||q||^2, x += a phat, r -= a q,
+    // z = P^{-T} A^T r, beta = ||z||^2 / gamma, p = z + beta p.  The four applications
+    // (h = 2: A^T, 3: P^{-T}, 0: P^{-1}, 1: A) share one inlined apply; the loop enters at h = 2
+    // with r = g already in A (rhs_phase).
     const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
     const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
-    // z = P^{-T} (A^T r): A^T on the padded input, then P^{-T} on its first npc values
-    auto ktrans = [&]() -> const double2 * {
-      const double2 *Z = apply<C, STG>(sm, P.L1e, ge, opAT, tw, r, xs);
-      if (!prec) return Z;
-      if (Z != sm.A) {
-        TSF_FOR_E(npc) { sm.A[pidx(e)] = Z[pidx(e)]; }
+    double gam = 0.0, a = 0.0;
+    bool first = true;
+    for (int h = 2;; h = (h + 1) & 3) {
+      const bool isP = !(h & 1);                // h = 0: P^{-1}, h = 2: A^T
+      const bool isPre = h == 0 || h == 3;
+      if (isPre && !prec) {
+        Y = sm.A;
+      } else {
         __syncthreads();
+        const SpecOp op = h == 0 ? opP : (h == 1 ? opA : (h == 2 ? opAT : opPT));
+        const Geo g = isPre ? gp : ge;
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
       }
-      return apply<C, STG>(sm, P.L1e, gp, opPT, tw, r, xs);
-    };
-    // A[0..npc) holds r = g and A[npc..) is zero (rhs_phase)
-    __syncthreads();
-    Y = ktrans();
-    double gz[1] = {0.0};
-    TSF_FOR_E(npc) {
-      const double2 z = Y[pidx(e)];
-      PV[e] = z;
-      gz[0] += cdot(z, z);
-    }
-    csum<C, 1>(gz, sm, xs);
-    double gam = gz[0];
-    double beta = 0.0;
-    for (int it = 0;; ++it) {
-      // Phase A: p = z + beta p; phat = P^{-1} p; q = A phat; ||q||^2
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = PV[e]; }, [&](int e, T1 &t) {
-        double2 pv = t.a;
-        if (it != 0) { pv = caxpy(beta, t.a, Y[pidx(e)]); PV[e] = pv; }
-        sm.A[pidx(e)] = pv;
-      });
-      __syncthreads();
-      Y = prec ? apply<C, STG>(sm, P.L1e, gp, opP, tw, r, xs) : sm.A;
-      TSF_FOR_E(npc) {
-        const double2 ph = Y[pidx(e)];
-        PH[e] = ph;
-        sm.A[pidx(e)] = ph;
-        sm.A[pidx(e + npc)] = zero2();
+      (void)isP;
+      if (h == 2) {                            // A^T r -> first npc values into A for P^{-T}
+        TSF_FOR_E(npc) {
+          const double2 v = Y[pidx(e)];
+          sm.A[pidx(e)] = v;
+        }
+        continue;
       }
-      __syncthreads();
-      Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+      if (h == 3) {                            // z = P^{-T} A^T r; gamma, beta; p = z + beta p
+        double zz[1] = {0.0};
+        TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+        csum<C, 1>(zz, sm, xs);
+        const double beta = first ? 0.0 : zz[0] / gam;
+        gam = zz[0];
+        TSF_FOR_E(npc) {
+          const double2 z = Y[pidx(e)];
+          const double2 pv = first ? z : caxpy(beta, PV[e], z);
+          PV[e] = pv;
+          sm.A[pidx(e)] = pv;
+        }
+        first = false;
+        continue;
+      }
+      if (h == 0) {                            // phat
+        TSF_FOR_E(npc) {
+          const double2 ph = Y[pidx(e)];
+          PH[e] = ph;
+          sm.A[pidx(e)] = ph;
+          sm.A[pidx(e + npc)] = zero2();
+        }
+        continue;
+      }
+      // h == 1: q = A phat; a = gamma / ||q||^2; x += a phat; r -= a q; ||r||
       double qq[1] = {0.0};
       TSF_FOR_E(npc) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
       csum<C, 1>(qq, sm, xs);
       if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      const double a = gam / qq[0];
-      // Phase B: x += a phat; r -= a q; ||r||; z = P^{-T} A^T r; ||z||^2
+      a = gam / qq[0];
       double rl[1] = {0.0};
-      batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = X[e]; t.b = PH[e]; t.c = R[e]; }, [&](int e, T3 &t) {
-        X[e] = caxpy(a, t.b, t.a);
-        const double2 rn = caxpy(-a, Y[pidx(e)], t.c);
+      TSF_FOR_E(npc) {
+        X[e] = caxpy(a, PH[e], X[e]);
+        const double2 rn = caxpy(-a, Y[pidx(e)], R[e]);
         R[e] = rn;
         sm.A[pidx(e)] = rn;
         sm.A[pidx(e + npc)] = zero2();
         rl[0] += cdot(rn, rn);
-      });
+      }
       csum<C, 1>(rl, sm, xs);
       hs += 2;
       relres = sqrt(rl[0] / rr0);
       if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
       if (relres < P.tol) break;
       if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
-      Y = ktrans();
-      double zz[1] = {0.0};
-      TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
-      csum<C, 1>(zz, sm, xs);
-      beta = zz[0] / gam;
-      gam = zz[0];
     }
   }
   if (mode != 0) {               // GSF setup: keep the solution of eq3.4

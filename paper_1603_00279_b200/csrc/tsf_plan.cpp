@@ -146,9 +146,9 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
     for (int c : cands) {
       if (!cluster_ok(n, c)) continue;
       if (C < 0) { C = c; continue; }            // smallest feasible cluster
-      // a larger cluster only while the GPU is not yet full and each CTA keeps
-      // >= 512 local FFT points (otherwise barriers dominate)
-      if (int64_t(B) * c <= 148 && n / c >= 512) C = c;
+      // a larger cluster only while the GPU is not yet full and each CTA keeps >= 256 local
+      // FFT points (measured at n = 1024: C = 2 / 4 / 8 -> 7.1k / 8.4k / 6.8k levels/s)
+      if (int64_t(B) * c <= 148 && n / c >= 256) C = c;
     }
     if (C < 0) return fail("no feasible cluster size for n=%g", double(n));
   } else {

@@ -96,6 +96,7 @@ def test_planner_cluster_choices_and_workspace():
     c3 = tsf.plan(config_c3())
     c4 = tsf.plan(config_c4(B=256))
     assert c1.cluster == 1 and c3.cluster == 16 and c4.cluster == 1
+    assert tsf.plan(CONFIGS["C2"]()).cluster == 4          # >= 256 local points per CTA
     assert c3.embed_len == 16384 and c3.precond_len == 8192
     # workspace grows with the history (M n doubles per instance) and the batch
     assert tsf.plan(config_c4(B=512)).workspace_bytes > c4.workspace_bytes

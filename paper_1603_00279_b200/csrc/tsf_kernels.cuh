@@ -713,23 +713,32 @@ struct Geo {
 };
 
 // C == 1: the whole transform is local; column pairs are bin pairs (k, L-k).  Slots come from
-// the exported slot table (L1-resident; measured faster here than the closed-form dslot).
+// the exported slot table (L1-resident; measured faster here than the closed-form dslot).  Two
+// pairs per thread and step, their table loads issued together (the loop is latency bound).
 __device__ __forceinline__ void pointwise_local(double2 *A, const Geo &g, const SpecOp &op,
                                              const double2 *__restrict__ tw) {
-  for (int i = threadIdx.x; i < g.np; i += kThreads) {
-    if (i == 0) {
-      const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
-      double2 a = A[sa], b = A[sb];
-      pair_self(a, op.get(0, 0, 0, 0), op.nyqe, tw[0], op.scale);
-      const double2 lm = op.get(0, 1, 0, g.L / 2);
-      pair_self(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
-      A[sa] = a; A[sb] = b;
-    } else {
-      const int sa = pidx(g.slot[i]), sb = pidx(g.slot[g.L1 - i]);
-      double2 a = A[sa], b = A[sb];
-      pair_apply(a, b, op.get(0, 0, i, i), op.get(0, 1, i, g.L - i), tw[i * g.tw2L], op.scale);
-      A[sa] = a; A[sb] = b;
-    }
+  if (threadIdx.x == 0) {
+    const int sa = pidx(g.slot[0]), sb = pidx(g.slot[g.L1 / 2]);
+    double2 a = A[sa], b = A[sb];
+    pair_self(a, op.get(0, 0, 0, 0), op.nyqe, tw[0], op.scale);
+    const double2 lm = op.get(0, 1, 0, g.L / 2);
+    pair_self(b, lm, lm, tw[(g.L / 2) * g.tw2L], op.scale);
+    A[sa] = a; A[sb] = b;
+  }
+  for (int i0 = threadIdx.x + 1; i0 < g.np; i0 += 2 * kThreads) {
+    const int i1 = i0 + kThreads;
+    const bool h1 = i1 < g.np;
+    const int j1 = h1 ? i1 : i0;
+    const double2 la0 = op.get(0, 0, i0, i0), lb0 = op.get(0, 1, i0, g.L - i0);
+    const double2 la1 = op.get(0, 0, j1, j1), lb1 = op.get(0, 1, j1, g.L - j1);
+    const double2 w0 = tw[i0 * g.tw2L], w1 = tw[j1 * g.tw2L];
+    const int sa0 = pidx(g.slot[i0]), sb0 = pidx(g.slot[g.L1 - i0]);
+    const int sa1 = pidx(g.slot[j1]), sb1 = pidx(g.slot[g.L1 - j1]);
+    double2 a0 = A[sa0], b0 = A[sb0], a1 = A[sa1], b1 = A[sb1];
+    pair_apply(a0, b0, la0, lb0, w0, op.scale);
+    pair_apply(a1, b1, la1, lb1, w1, op.scale);
+    A[sa0] = a0; A[sb0] = b0;
+    if (h1) { A[sa1] = a1; A[sb1] = b1; }
   }
 }
 

@@ -67,6 +67,7 @@ struct Inst {
   double *vec, *hist;
   double2 *mul;          // per-level multiplier tables [n + n/2] (task order), HBM variant
   double2 *gsf;          // NEXT-2: spectra of the 4 triangular GSF factors [4][n+1] (task order)
+  double2 *xg;           // unstaged clusters: L2 exchange buffer [C][L1e] of the local FFT outputs
   int32_t *it, *st;
   double *rr;
 };
@@ -88,6 +89,7 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.hist = reinterpret_cast<double *>(base + P.o_hist);
   I.mul = reinterpret_cast<double2 *>(base + P.o_mul);
   I.gsf = reinterpret_cast<double2 *>(base + P.o_gsf);
+  I.xg = reinterpret_cast<double2 *>(base + P.o_xg);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
   I.st = reinterpret_cast<int32_t *>(base + P.o_st);
@@ -896,17 +898,20 @@ __device__ __forceinline__ void col_twiddles(double2 w, double2 (&wq)[C]) {
 // push before the local inverse FFTs.
 template <int C>
 __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, const Geo &g, const SpecOp &op,
-                                              const double2 *__restrict__ tw, uint32_t r, const Smem &sm) {
+                                              const double2 *__restrict__ tw, uint32_t r, const Smem &sm,
+                                              const double2 *__restrict__ xg) {
   TSF_PT0();
   const int L1 = g.L1, np = g.np, l1 = g.l1;
   const int W = 2 * CP;                       // columns per chunk
   for (int c0 = 0; c0 < np; c0 += CP) {
     const int cp = np - c0 < CP ? np - c0 : CP;
-    // pull: item u -> (row q, chunk column col)
+    // pull: item u -> (row q, chunk column col); the rows come from the peers' local FFT outputs
+    // staged in L2 (xg[q][slot], written by the caller before its cluster barrier): ~10x the
+    // per-SM bandwidth of DSMEM loads (measured 6-10 B/clk/SM)
     for (int u = threadIdx.x; u < C * 2 * cp; u += kThreads) {
       const int q = u / (2 * cp), col = u - q * (2 * cp);
       const int k1 = col_k1(L1, C, r, 2 * c0 + col);
-      Bc[q * W + col] = remote<C>(A, uint32_t(q))[pidx(dslot(k1, l1))];
+      Bc[q * W + col] = __ldcg(xg + q * L1 + dslot(k1, l1));
     }
     __syncthreads();
     TSF_PACC(sm, PS_GATHER);
@@ -1010,7 +1015,8 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
 #endif
 template <int C, bool STG>
 __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
-                                       const double2 *__restrict__ tw, uint32_t r, Xch &xs) {
+                                       const double2 *__restrict__ tw, uint32_t r, Xch &xs,
+                                       double2 *xg = nullptr) {
   TSF_PT0();
   local_fft<false>(sm.A, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_F);
@@ -1024,9 +1030,10 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
       cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs);
       Y = sm.O;
     } else {
-      csync<C>();                // every local transform done before remote gathers
+      for (int p = threadIdx.x; p < g.L1; p += kThreads) xg[int64_t(r) * g.L1 + p] = sm.A[pidx(p)];
+      csync<C>();                // every local transform staged in L2 before the gathers
       TSF_PACC(sm, PS_BAR1);
-      cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r, sm);
+      cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r, sm, xg);
       csync<C>();                // every push landed before the local inverse transforms
       TSF_PACC(sm, PS_BAR3);
     }
@@ -1287,7 +1294,7 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
     sm.A[pidx(e + npc)] = zero2();
   }
   __syncthreads();
-  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs);
+  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs, I.xg);
   double acc = 0.0;
   TSF_FOR_E(npc) {
     double2 g = Y[pidx(e)];
@@ -1335,7 +1342,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
     }
     __syncthreads();
     const SpecOp op = make_gsf_op(P, I, k, r, sm);
-    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs);
+    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
     double2 *Z = k == 0 ? Z1 : Z2;
     TSF_FOR_E(npc) { Z[e] = Y[pidx(e)]; }
   }
@@ -1348,7 +1355,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
     }
     __syncthreads();
     const SpecOp op = make_gsf_op(P, I, k, r, sm);
-    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs);
+    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
     if (k == 2) {
       TSF_FOR_E(npc) { X[e] = Y[pidx(e)]; }
     } else {
@@ -1362,7 +1369,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
   }
   __syncthreads();
   const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
-  Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs);
+  Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs, I.xg);
   double rs[1] = {0.0};
   TSF_FOR_E(npc) {
     const double2 d = csub(Y[pidx(e)], G[e]);
@@ -1463,7 +1470,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         __syncthreads();
         const SpecOp op = isP ? opP : opA;
         const Geo g = isP ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
       }
       if (isP) {
         // h = 0: phat = Y; h = 2: shat = Y.  Either becomes the (padded) input of A.
@@ -1562,7 +1569,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         __syncthreads();
         const SpecOp op = isP ? opP : opA;
         const Geo g = isP ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
       }
       if (h == 0) {                            // phat
         TSF_FOR_E(npc) {
@@ -1641,7 +1648,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         __syncthreads();
         const SpecOp op = h == 0 ? opP : (h == 1 ? opA : (h == 2 ? opAT : opPT));
         const Geo g = isPre ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs);
+        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
       }
       (void)isP;
       if (h == 2) {                            // A^T r -> first npc values into A for P^{-T}
@@ -1871,7 +1878,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
     }
     __syncthreads();
     const SpecOp op = make_op(P, I, j, wh, r, sm);
-    Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs);
+    Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs, I.xg);
   }
   for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
 #ifdef TSF_PROFILE

@@ -219,6 +219,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.o_st = q;    q = up(q + size_t(P.M) * 4);
   P.o_mul = q;   q = up(q + size_t(n + n / 2) * 16);
   P.o_gsf = q;   q = up(q + (s->method == TSF_GSF ? size_t(4) * size_t(n + 1) * 16 : 0));
+  P.o_xg = q;    q = up(q + (C > 1 && !P.staged ? size_t(n) * 16 : 0));   // L2 exchange (unstaged)
   P.stride = q;
   P.total = P.off_inst + P.stride * size_t(B);
   *pl = P;
@@ -339,7 +340,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.o_par = pl.o_par; d.o_omega = pl.o_omega; d.o_lwe = pl.o_lwe; d.o_lwp = pl.o_lwp;
   d.o_lev = pl.o_lev; d.o_hwc = pl.o_hwc; d.o_hwe = pl.o_hwe; d.o_scal = pl.o_scal;
   d.o_basis = pl.o_basis; d.o_ftab = pl.o_ftab; d.o_vec = pl.o_vec; d.o_hist = pl.o_hist;
-  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf;
+  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
   return d;
 }
 

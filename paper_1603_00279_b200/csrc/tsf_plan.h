@@ -55,7 +55,7 @@ struct DevParams {
   char *inst;                      // base of instance 0
   int64_t stride;                  // bytes between instances
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf, o_xg;
 };
 
 struct Plan {
@@ -77,7 +77,7 @@ struct Plan {
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf;
+  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf, o_xg;
 };
 
 // Per-instance host tables (all doubles).

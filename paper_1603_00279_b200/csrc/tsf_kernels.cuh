@@ -531,11 +531,88 @@ __device__ __forceinline__ void fft_pass16(double2 *A, int L1, int lm, const Sme
   }
 }
 
+// Compile-time-specialised radix-4 plan for the resident (direct twiddle table) lengths of the
+// C3 cluster kernels: all index arithmetic folds to shifts/masks of constants (same data
+// placement as local_fft).
+template <bool INV, int LM>
+__device__ __forceinline__ void st4_ct(double2 *A, int L1, const double2 *twd, int L1e) {
+  constexpr int lmp = LM - 2, mprev = 1 << lmp;
+  const int tstep = L1e >> LM;
+  const int nb = L1 >> 2;
+  for (int b = threadIdx.x; b < nb; b += kThreads) {
+    const int k = b & (mprev - 1);
+    const int base = ((b >> lmp) << LM) + k;
+    const int p0 = pidx(base), p1 = pidx(base + mprev), p2 = pidx(base + 2 * mprev), p3 = pidx(base + 3 * mprev);
+    double2 a0 = A[p0], a1 = A[p1], a2 = A[p2], a3 = A[p3];
+    const double2 w1 = twd[k * tstep];
+    const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+    if (INV) {
+      a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
+      bfly4<true>(a0, a1, a2, a3);
+    } else {
+      bfly4<false>(a0, a1, a2, a3);
+      a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
+    }
+    A[p0] = a0; A[p1] = a1; A[p2] = a2; A[p3] = a3;
+  }
+}
+template <bool INV, int L, int S>   // radix-4 stages S-1 .. 0 (DIF) or 0 .. S-1 (DIT)
+struct Ct4 {
+  __device__ __forceinline__ static void run(double2 *A, const double2 *twd, int L1e) {
+    if constexpr (S > 0) {
+      if constexpr (!INV) {
+        st4_ct<false, 2 * S>(A, L, twd, L1e);
+        __syncthreads();
+        Ct4<INV, L, S - 1>::run(A, twd, L1e);
+      } else {
+        Ct4<INV, L, S - 1>::run(A, twd, L1e);
+        st4_ct<true, 2 * S>(A, L, twd, L1e);
+        __syncthreads();
+      }
+    }
+  }
+};
+template <bool INV, int L>
+__device__ __forceinline__ void local_fft_ct(double2 *A, const double2 *twd, int L1e) {
+  constexpr int l = __builtin_ctz(L), S4 = l / 2;
+  constexpr bool r2 = l & 1;
+  if constexpr (!INV) {
+    if constexpr (r2) {
+      for (int b = threadIdx.x; b < L / 2; b += kThreads) {
+        const int p0 = pidx(b), p1 = pidx(b + L / 2);
+        const double2 a0 = A[p0], a1 = A[p1];
+        A[p0] = cadd(a0, a1);
+        A[p1] = cmul(csub(a0, a1), twd[b * (L1e / L)]);
+      }
+      __syncthreads();
+    }
+    Ct4<false, L, S4>::run(A, twd, L1e);
+  } else {
+    Ct4<true, L, S4>::run(A, twd, L1e);
+    if constexpr (r2) {
+      for (int b = threadIdx.x; b < L / 2; b += kThreads) {
+        const int p0 = pidx(b), p1 = pidx(b + L / 2);
+        const double2 a0 = A[p0];
+        const double2 a1 = cmulc(A[p1], twd[b * (L1e / L)]);
+        A[p0] = cadd(a0, a1);
+        A[p1] = csub(a0, a1);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Requires the input to be visible to all threads (caller synchronizes); ends synchronized.
 // Radix-4 stages are fused pairwise into radix-16 register passes from the bottom (stages
 // (1,0), (3,2), ...); a leftover top radix-4 stage and the radix-2 stage run alone.
 template <bool INV>
 __device__ __forceinline__ void local_fft(double2 *A, int L1, const Smem &sm, int L1e) {
+#ifndef TSF_NO_CT_FFT
+  if (sm.twd != nullptr && L1e == 1024) {       // C3's resident cluster kernels (n = 2^14, C = 16)
+    if (L1 == 1024) { local_fft_ct<INV, 1024>(A, sm.twd, L1e); return; }
+    if (L1 == 512) { local_fft_ct<INV, 512>(A, sm.twd, L1e); return; }
+  }
+#endif
   const int l = __ffs(L1) - 1;
   const int S4 = l >> 1;
   const bool r2 = l & 1;

@@ -102,7 +102,7 @@ def test_spectra_match_direct_ffts_of_the_oracle_generators(precond, n, cluster)
 
 
 @pytest.mark.parametrize("n,cluster", [(64, 1), (256, 1), (1024, 2), (1024, 4), (1024, 8), (1024, 16),
-                                       (4096, 1), (4096, 8), (4096, 16)])
+                                       (2048, 2), (4096, 1), (4096, 4), (4096, 8), (4096, 16)])
 def test_operator_applications_match_dense(n, cluster):
     from scipy.linalg import circulant
     inst, p = pair(0.7, 1.6, n, 8, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),

@@ -612,6 +612,10 @@ __device__ __forceinline__ void local_fft(double2 *A, int L1, const Smem &sm, in
     if (L1 == 1024) { local_fft_ct<INV, 1024>(A, sm.twd, L1e); return; }
     if (L1 == 512) { local_fft_ct<INV, 512>(A, sm.twd, L1e); return; }
   }
+  if (sm.twd != nullptr && L1e == 256) {        // C2's (n = 2^10, C = 4)
+    if (L1 == 256) { local_fft_ct<INV, 256>(A, sm.twd, L1e); return; }
+    if (L1 == 128) { local_fft_ct<INV, 128>(A, sm.twd, L1e); return; }
+  }
 #endif
   const int l = __ffs(L1) - 1;
   const int S4 = l >> 1;

@@ -26,9 +26,10 @@ SRC_ZERO, SRC_TABLE, SRC_EXA, SRC_MMS3 = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (-O2, no FMA contraction: DESIGN.md R-fma)."""
+    """Compile liboracle.so with gcc (-O2, no FMA contraction: DESIGN.md R-fma; -fopenmp over
+    independent rows only, bitwise identical for any thread count)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-std=c99",
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c99",
                "-D_GNU_SOURCE", _SRC, "-o", _LIB + ".tmp", "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)

@@ -7,7 +7,10 @@
  * blocking, fusion or reordering beyond what the paper's definitions state.
  *
  * Built with -O2 -ffp-contract=off (reading R-fma): IEEE round-to-nearest,
- * no fused multiply-add, so results are reproducible across hosts.
+ * no fused multiply-add, so results are reproducible across hosts.  -fopenmp splits the
+ * independent ROWS of the dense loops (assembly, products, the GE row updates, refinement
+ * residuals) across threads; every row's arithmetic and summation order is unchanged, so
+ * results are bitwise identical for any OMP_NUM_THREADS (tests/test_oracle.py checks it).
  */
 #include "oracle.h"
 #include <math.h>
@@ -113,6 +116,7 @@ static void dense_L(const orc_problem *p, int64_t j, double *L) {
   const double hb = pow(h, p->beta);
   double *omega = (double *)malloc(sizeof(double) * (size_t)(n + 2));
   orc_wsgd(p->beta, n + 1, omega);
+#pragma omp parallel for schedule(static) if (n > 256)
   for (int64_t i = 0; i < n; ++i)
     for (int64_t m = 0; m < n; ++m) {
       double W = (i - m + 1 >= 0) ? omega[i - m + 1] : 0.0;   /* W[i][m]   */
@@ -130,6 +134,7 @@ int orc_assemble(const orc_problem *p, int64_t j, double *A, double *B) {
   const double sigma = 1.0 - p->alpha / 2.0;
   const double eta = orc_eta(p->alpha, tau, j);
   dense_L(p, j, A);
+#pragma omp parallel for schedule(static) if (n > 256)
   for (int64_t i = 0; i < n; ++i)
     for (int64_t m = 0; m < n; ++m) {
       const double Lim = A[i * n + m];
@@ -217,6 +222,9 @@ static int lu_factor(int64_t n, double *A, int64_t *piv) {
         double tmp = A[k * n + m]; A[k * n + m] = A[pr * n + m]; A[pr * n + m] = tmp;
       }
     const double inv = 1.0 / A[k * n + k];
+    /* rows are independent: OpenMP splits them across threads, each row's arithmetic is
+     * unchanged, so the factors are bitwise identical to the single-threaded loop */
+#pragma omp parallel for schedule(static) if (n - k > 256)
     for (int64_t i = k + 1; i < n; ++i) {
       const double l = A[i * n + k] * inv;
       A[i * n + k] = l;
@@ -254,6 +262,7 @@ static void refine(int64_t n, const double *A0, const double *LU, const int64_t 
                    const double *b, double *x, int steps) {
   double *d = (double *)malloc(sizeof(double) * (size_t)n);
   for (int it = 0; it < steps; ++it) {
+#pragma omp parallel for schedule(static) if (n > 256)
     for (int64_t i = 0; i < n; ++i) {
       long double s = (long double)b[i];
       const double *ai = A0 + i * n;
@@ -294,6 +303,7 @@ static void rhs_with_B(const orc_problem *p, int64_t j, const double *U, const d
   const double sigma = 1.0 - p->alpha / 2.0;
   const double kappa = pow(tau, -p->alpha) / tgamma(2.0 - p->alpha);
   const double *uj = U + j * n;
+#pragma omp parallel for schedule(static) if (n > 256)
   for (int64_t i = 0; i < n; ++i) {
     double s = 0.0;
     for (int64_t m = 0; m < n; ++m) s += B[i * n + m] * uj[m];
@@ -328,7 +338,10 @@ int orc_rhs(const orc_problem *p, int64_t j, const double *U, double *g) {
 
 /* Matrix-free products with A^{(j+sigma)} (which = 0) or B^{(j+sigma)} (which = 1): the
  * same entries as orc_assemble (eq3.2-eq3.3) generated row by row, O(n^2) time and O(n)
- * memory, for sampled checks at sizes where the dense matrix does not fit.               */
+ * memory, for sampled checks at sizes where the dense matrix does not fit.  Each row sum is
+ * accumulated in x87 extended precision, as the refinement residuals are (R-refine): at
+ * n = 2^17 the entries reach h^{-beta} ~ 1e10 and cancel to O(1), so a double accumulator
+ * would add its own ~1e-6 relative error to a residual check of that size.              */
 int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y) {
   if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
   const int64_t n = p->n;
@@ -343,15 +356,16 @@ int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, doub
   const double mu = (which == 0) ? -sigma : (1.0 - sigma);
   double *omega = (double *)malloc(sizeof(double) * (size_t)(n + 2));
   orc_wsgd(p->beta, n + 1, omega);
+#pragma omp parallel for schedule(static) if (n > 256)
   for (int64_t i = 0; i < n; ++i) {
-    double s = 0.0;
+    long double s = 0.0L;
     for (int64_t m = 0; m < n; ++m) {
       double W = (i - m + 1 >= 0) ? omega[i - m + 1] : 0.0;
       double WT = (m - i + 1 >= 0) ? omega[m - i + 1] : 0.0;
       double Q = (m == i + 1) ? 1.0 : ((m == i - 1) ? -1.0 : 0.0);
-      s += (gam / (2.0 * h) * Q + dp / hb * W + dm / hb * WT) * x[m];
+      s += (long double)(gam / (2.0 * h) * Q + dp / hb * W + dm / hb * WT) * (long double)x[m];
     }
-    y[i] = eta * x[i] + mu * s;
+    y[i] = (double)((long double)eta * (long double)x[i] + (long double)mu * s);
   }
   free(omega);
   return 0;

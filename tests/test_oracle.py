@@ -488,3 +488,49 @@ def test_embedding_matvec_equals_dense():
     x = rng.standard_normal(16)
     y = np.fft.ifft(np.fft.fft(e) * np.fft.fft(np.r_[x, np.zeros(16)]))[:16].real
     np.testing.assert_allclose(y, A @ x, rtol=1e-12, atol=1e-10)
+
+
+# ------------------------------------------------------------------ matrix-free oracle (full-size checker)
+@pytest.mark.parametrize("n", [9, 33, 64])
+@pytest.mark.parametrize("j", [0, 1, 6])
+def test_matrix_free_products_match_delta_operator_and_dense(n, j):
+    """orc_matvec / orc_rhs_nodense are the checkers at sizes where no dense matrix fits (C3,
+    C5).  Pinned to the literal delta_h^beta operator of P:310-312 (A = eta I - sigma D,
+    B = eta I + (1-sigma) D, eq3.3) and to the dense RHS of alg1 step 2."""
+    p = O.Problem(alpha=0.7, beta=1.6, n=n, M=8, gamma=(O.COS, 0.7), dplus=(O.ONE_PLUS_T, 1.3),
+                  dminus=(O.ONE_PLUS_T2, 0.4), src=O.SRC_MMS3)
+    D = _delta_matrix(p, j)
+    eta, sigma = O.eta(p.alpha, p.tau, j), p.sigma
+    x = np.random.default_rng(n + j).standard_normal(n)
+    for which, Mx in ((0, eta * np.eye(n) - sigma * D), (1, eta * np.eye(n) + (1 - sigma) * D)):
+        y = O.matvec(p, j, which, x)
+        assert np.linalg.norm(y - Mx @ x) <= 1e-13 * np.linalg.norm(Mx @ x)
+        A, B = O.assemble(p, j)
+        assert np.linalg.norm(y - (A if which == 0 else B) @ x) <= 1e-13 * np.linalg.norm(y)
+    U = O.solve(p)
+    g = O.rhs_nodense(p, j, U[: j + 1])
+    ref = O.rhs(p, j, U[: j + 1])
+    assert np.linalg.norm(g - ref) <= 1e-13 * np.linalg.norm(ref)
+    # the level solution satisfies the matrix-free system (ties both to the GE path)
+    assert np.linalg.norm(O.matvec(p, j, 0, U[j + 1]) - g) <= 1e-12 * np.linalg.norm(g)
+
+
+def test_openmp_rows_are_bitwise_thread_independent():
+    """oracle.c splits independent rows across OpenMP threads; the results must not depend on
+    the thread count (every row's summation order is fixed)."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, oracle as O\n"
+            "p = O.Problem(alpha=0.8, beta=1.8, n=600, M=3, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),"
+            " dminus=(O.ONE_PLUS_T2, 1.0), src=O.SRC_MMS3)\n"
+            "U = O.solve(p)\n"
+            "print(U.tobytes().hex()[:0] + str(hash(U.tobytes())) + ' ' +"
+            " str(hash(O.matvec(p, 1, 0, U[2]).tobytes())))\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for th in ("1", "3", "8"):
+        env = dict(os.environ, OMP_NUM_THREADS=th, PYTHONPATH=root, PYTHONHASHSEED="0")
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                   text=True, check=True).stdout.strip())
+    assert outs[0] == outs[1] == outs[2], outs

@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-true-res", action="store_true", help="skip the per-level true residual")
+    ap.add_argument("--warm", action="store_true", help="NEXT-3 warm start x0 = u^j")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -272,7 +274,8 @@ def main():
 
     insts, scaling, units_total = build_instances(args.config, world, rank)
     n, M = insts[0].n, insts[0].M
-    solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster)
+    solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster,
+                     true_residual=not args.no_true_res, x0_warm=args.warm)
     stream = torch.cuda.Stream(dev)
     t_init0 = time.perf_counter()
     s = tsf.Solver(insts, stream=stream, **solver_kw)

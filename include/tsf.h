@@ -63,10 +63,13 @@ extern "C" {
  * true residual ||A u - g|| / ||g||. */
 typedef enum { TSF_BICGSTAB = 0, TSF_CGNR = 1, TSF_PCGS = 2, TSF_GSF = 3 } tsf_method;
 typedef enum { TSF_STRANG = 0, TSF_TCHAN = 1, TSF_NOPREC = 2 } tsf_precond;
-typedef enum { TSF_SRC_ZERO = 0, TSF_SRC_SEPARABLE = 1, TSF_SRC_TABLE = 2 } tsf_src_kind;
+typedef enum { TSF_SRC_ZERO = 0, TSF_SRC_SEPARABLE = 1, TSF_SRC_TABLE = 2, TSF_SRC_CALLBACK = 3 } tsf_src_kind;
 
 /* host scalar function of time or space; evaluated on the host during tsf_init only */
 typedef double (*tsf_fn_t)(double arg, void *ctx);
+/* host source callback (general f of eq:lin): out[i] = f(x[i], t) for the n interior
+ * nodes x at time t = t_{j+sigma}; called once per level during tsf_init (slow path). */
+typedef void (*tsf_src_cb)(const double *x, int64_t n, double t, double *out, void *ctx);
 
 /* One problem instance (eq:lin).  Coefficients: for each of gamma, d+, d- give EITHER a
  * host array of M samples at t_{j+sigma} (the points tsf_sample_points returns) OR a host
@@ -75,7 +78,13 @@ typedef double (*tsf_fn_t)(double arg, void *ctx);
  * Source f^{j+sigma}_i = f(x_i, t_{j+sigma}):
  *   TSF_SRC_ZERO      f = 0
  *   TSF_SRC_SEPARABLE f^{j+sigma} = sum_{k<K} scal[j*K+k] * basis[k*n+i], 1 <= K <= 4
- *   TSF_SRC_TABLE     f^{j+sigma}_i = f_table[j*n+i]  (host array, M x n)              */
+ *   TSF_SRC_TABLE     f^{j+sigma}_i = f_table[j*n+i]  (M x n, natural order): a host array
+ *                     (copied at init), or with f_table_on_device = 1 a device array of the
+ *                     handle's device that is BORROWED (read every level; must stay valid and
+ *                     unchanged until tsf_destroy; all instances of a handle agree on the flag)
+ *   TSF_SRC_CALLBACK  f^{j+sigma} = f_cb(x, n, t_{j+sigma}) evaluated on the host once per level
+ *                     during tsf_init into the instance's device table; a non-finite value
+ *                     makes tsf_init fail with TSF_E_ARG                                    */
 typedef struct {
   double alpha, beta;
   int64_t n;
@@ -91,17 +100,27 @@ typedef struct {
   int32_t K;
   const double *basis;                          /* host [K][n] */
   const double *scal;                           /* host [M][K] */
-  const double *f_table;                        /* host [M][n] */
+  const double *f_table;                        /* [M][n], host (or device, see below) */
+  int32_t f_table_on_device;                    /* 1: f_table is borrowed device memory  */
+  tsf_src_cb f_cb;                              /* TSF_SRC_CALLBACK                      */
+  void *f_ctx;
 } tsf_problem;
 
 /* Solver settings.  tol = 1e-12 and x0 = 0 follow P:922-925.  cluster: CTAs cooperating
- * on one instance (thread-block cluster), 0 = planner's choice, else 1/2/4/8/16. */
+ * on one instance (thread-block cluster), 0 = planner's choice, else 1/2/4/8/16.
+ * x0_warm (NEXT-3, SPEC open question S:321): 0 = the paper's x0 = 0 with the stop
+ * ||r_k|| < tol ||r_0|| = tol ||g||; 1 = initial guess u^j (one extra A application per level,
+ * r_0 = g - A u^j) with the same g-relative stop ||r_k|| < tol ||g||.  Not for TSF_GSF.
+ * true_residual: 1 = at every level exit also compute ||g - A u^{j+1}|| / ||g|| with a fresh
+ * operator application (tsf_get_true_residuals; SURVEY reading c13), 0 = skip it. */
 typedef struct {
   int32_t method;     /* tsf_method  */
   int32_t precond;    /* tsf_precond */
   double tol;         /* > 0 */
   int32_t maxit;      /* > 0; 1000 BiCGSTAB / PCGS, 5000 CGNR */
   int32_t cluster;
+  int32_t x0_warm;
+  int32_t true_residual;
 } tsf_solver;
 
 /* Plan summary (host only, no GPU needed). */
@@ -112,6 +131,11 @@ typedef struct {
   int64_t embed_len;          /* complex FFT length of the 2n real embedding (= n)     */
   int64_t precond_len;        /* complex FFT length of the n-point preconditioner (n/2)*/
   size_t workspace_bytes;     /* device workspace required                             */
+  int32_t exchange;           /* cross-CTA column stage: 0 none (cluster 1), 1 staged
+                                 DSMEM push (local length <= 4096), 2 chunked through L2  */
+  int32_t chunk;              /* exchange 2: column pairs per chunk                     */
+  int32_t vsmem;              /* 1: Krylov vectors kept in shared memory, 0: in HBM     */
+  int32_t resident;           /* 1: per-level multiplier/twiddle tables in shared memory*/
 } tsf_plan_info;
 
 typedef struct tsf_handle tsf_handle;
@@ -156,6 +180,10 @@ int tsf_get_solutions(tsf_handle *h, double *out, int32_t out_on_device);
  * iters_half = Krylov iterations x 2 (a BiCGSTAB half-step exit counts 1), relres = final
  * recurrence ||r||/||r0||, status = TSF_LEVEL_*.  Entries of levels not yet run are 0.  */
 int tsf_get_stats(tsf_handle *h, int32_t *iters_half, double *relres, int32_t *status);
+/* True relative residuals ||g^{j+1} - A u^{j+1}|| / ||g^{j+1}|| of every level, host array
+ * [B][M] (0 for levels not yet run or when the solver's true_residual was 0; the GSF path
+ * always stores it).  Synchronizes the stream. */
+int tsf_get_true_residuals(tsf_handle *h, double *true_relres);
 /* Plan actually used by the handle. */
 int tsf_handle_info(const tsf_handle *h, tsf_plan_info *info);
 /* Release host resources (the workspace belongs to the caller). */
@@ -196,6 +224,10 @@ int tsf_debug_rhs(tsf_handle *h, int32_t inst, double *out);
 /* Overwrite the solution history of instance `inst` with host U[(j+1)][n] = u^0..u^j and
  * set the handle to level j (teacher forcing).  Every instance is moved to level j.    */
 int tsf_debug_set_history(tsf_handle *h, int32_t inst, int64_t j, const double *U);
+/* History-helper handshake words of the last solve (out[8] host): [0] solver CTA-levels done,
+ * [1..2] ready[J&1], [3..4] helper counters, [5] 1 if a bounded wait timed out and the solver
+ * summed the history itself. */
+int tsf_debug_helper_state(tsf_handle *h, int64_t *out);
 /* Section cycle counters of the profiling build (libtsf_prof.so; zeros otherwise):
  * out[32] host, then cleared when reset != 0.                                          */
 int tsf_debug_prof(tsf_handle *h, uint64_t *out, int32_t reset);

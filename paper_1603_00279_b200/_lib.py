@@ -20,9 +20,10 @@ ERRORS = {-1: "TSF_E_ARG", -2: "TSF_E_WORKSPACE", -3: "TSF_E_CUDA", -4: "TSF_E_S
           -5: "TSF_E_BREAKDOWN", -6: "TSF_E_DIVERGED", -7: "TSF_E_STATE"}
 BICGSTAB, CGNR, PCGS, GSF = 0, 1, 2, 3
 STRANG, TCHAN, NOPREC = 0, 1, 2
-SRC_ZERO, SRC_SEPARABLE, SRC_TABLE = 0, 1, 2
+SRC_ZERO, SRC_SEPARABLE, SRC_TABLE, SRC_CALLBACK = 0, 1, 2, 3
 
 FN_T = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
+SRC_CB = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int64, C.c_double, C.POINTER(C.c_double), C.c_void_p)
 PD = C.POINTER(C.c_double)
 
 
@@ -33,18 +34,21 @@ class TsfProblem(C.Structure):
                 ("gamma_fn", FN_T), ("dplus_fn", FN_T), ("dminus_fn", FN_T), ("coef_ctx", C.c_void_p),
                 ("phi", PD), ("phi_fn", FN_T), ("phi_ctx", C.c_void_p),
                 ("src_kind", C.c_int32), ("K", C.c_int32),
-                ("basis", PD), ("scal", PD), ("f_table", PD)]
+                ("basis", PD), ("scal", PD), ("f_table", PD), ("f_table_on_device", C.c_int32),
+                ("f_cb", SRC_CB), ("f_ctx", C.c_void_p)]
 
 
 class TsfSolver(C.Structure):
     _fields_ = [("method", C.c_int32), ("precond", C.c_int32), ("tol", C.c_double),
-                ("maxit", C.c_int32), ("cluster", C.c_int32)]
+                ("maxit", C.c_int32), ("cluster", C.c_int32), ("x0_warm", C.c_int32),
+                ("true_residual", C.c_int32)]
 
 
 class TsfPlanInfo(C.Structure):
     _fields_ = [("cluster", C.c_int32), ("threads", C.c_int32), ("smem_bytes", C.c_int64),
                 ("embed_len", C.c_int64), ("precond_len", C.c_int64),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("exchange", C.c_int32), ("chunk", C.c_int32),
+                ("vsmem", C.c_int32), ("resident", C.c_int32)]
 
 
 class TsfError(RuntimeError):
@@ -70,6 +74,7 @@ _SIGS = {
     "tsf_get_solution": (C.c_int, [C.c_void_p, C.c_int32, PD, C.c_int32]),
     "tsf_get_solutions": (C.c_int, [C.c_void_p, PD, C.c_int32]),
     "tsf_get_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), PD, C.POINTER(C.c_int32)]),
+    "tsf_get_true_residuals": (C.c_int, [C.c_void_p, PD]),
     "tsf_handle_info": (C.c_int, [C.c_void_p, C.POINTER(TsfPlanInfo)]),
     "tsf_destroy": (C.c_int, [C.c_void_p]),
     "tsf_last_error": (C.c_char_p, []),
@@ -83,6 +88,7 @@ _SIGS = {
     "tsf_debug_rhs": (C.c_int, [C.c_void_p, C.c_int32, PD]),
     "tsf_debug_set_history": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, PD]),
     "tsf_debug_prof": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int32]),
+    "tsf_debug_helper_state": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -97,6 +103,8 @@ def load():
                               f"g.build()'` (nvcc, sm_100a)")
         lib = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if _VARIANT and not hasattr(lib, name):
+                continue          # developer variants (e.g. an older build) may lack new hooks
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

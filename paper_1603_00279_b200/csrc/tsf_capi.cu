@@ -3,6 +3,7 @@
 // level step, statistics and test hooks.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -184,19 +185,73 @@ __global__ void k_scatter_spec(DevParams P, int b0, int nb, const double2 *emb, 
 
 __global__ void k_reset(DevParams P) {
   const int64_t n = P.n;
-  const int64_t per = n + 3 * P.M;
+  const int64_t per = n + 4 * P.M;
   const int64_t total = per * P.B;
   for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total;
        id += int64_t(gridDim.x) * blockDim.x) {
     const int b = int(id / per);
     const int64_t k = id % per;
     Inst I = inst_view(P, b);
-    if (k < n) I.vec[V_U * n + k] = I.vec[V_PHI * n + k];
+    if (k < n) I.vec[V_U * n + k] = I.phi[k];
     else if (k < n + P.M) I.it[k - n] = 0;
     else if (k < n + 2 * P.M) I.rr[k - n - P.M] = 0.0;
-    else I.st[k - n - 2 * P.M] = 0;
+    else if (k < n + 3 * P.M) I.trr[k - n - 2 * P.M] = 0.0;
+    else I.st[k - n - 3 * P.M] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *P.level = 0;
+}
+
+// Nonsingularity guard of the circulant preconditioner (themx2 P:831-848 proves
+// P nonsingular in exact arithmetic): for every (instance, level) block, min and max |lambda_P|
+// over the n/2 + 1 bins of the level's spectrum; |lambda_P| < 1e-14 max |lambda_P| marks the
+// level TSF_LEVEL_SINGULAR_PREC (tsf_init then fails with TSF_E_SINGULAR_PREC).
+__global__ void k_prec_guard(DevParams P) {
+  const int b = int(blockIdx.x / P.M);
+  const int64_t j = blockIdx.x % P.M;
+  const Inst I = inst_view(P, b);
+  const Smem none = {};
+  const SpecOp op = make_op(P, I, j, OP_PINV, 0, none);
+  const int64_t half = P.n / 2;
+  const int C = P.C, np = P.npp;
+  double lo = INFINITY, hi = 0.0;
+  for (int64_t q = threadIdx.x; q <= half; q += blockDim.x) {
+    double2 l;
+    if (q == half) {
+      l = op.nyquist_lam(int(half));
+    } else {
+      const int i = int(q % np), ab = int((q / np) % 2), k2 = int((q / (2 * np)) % C);
+      const int r = int(q / (2 * np * C));
+      l = op.lam_idx(int(q), int(task_bin(P.L1p, C, r, i, k2, ab)));
+    }
+    const double m2 = l.x * l.x + l.y * l.y;
+    lo = fmin(lo, m2);
+    hi = fmax(hi, m2);
+  }
+  __shared__ double slo[32], shi[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { slo[threadIdx.x >> 5] = lo; shi[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) { lo = fmin(lo, slo[w]); hi = fmax(hi, shi[w]); }
+    lo = fmin(lo, slo[0]);
+    hi = fmax(hi, shi[0]);
+    if (!(lo >= 1e-28 * hi) || !(hi > 0.0)) I.st[j] = TSF_LEVEL_SINGULAR_PREC;   // |l| < 1e-14 max|l|
+  }
+}
+
+// u^j of instances [b0, b0 + nb) in natural order (device output of tsf_get_solution(s))
+__global__ void k_gather_u(DevParams P, int b0, int nb, double *out) {
+  const int64_t n = P.n;
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < int64_t(nb) * n;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int b = int(id / n);
+    const int64_t e = id % n;
+    const Inst I = inst_view(P, b0 + b);
+    out[id] = I.vec[V_U * n + perm_pos(n, P.C, e)];
+  }
 }
 
 __global__ void k_set_level(int64_t *level, int64_t v) {
@@ -387,6 +442,10 @@ int tsf_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, tsf_plan_info
     info->embed_len = pl.n;
     info->precond_len = pl.n / 2;
     info->workspace_bytes = pl.total;
+    info->exchange = pl.C == 1 ? 0 : (pl.staged ? 1 : 2);
+    info->chunk = pl.chunk;
+    info->vsmem = pl.vsmem;
+    info->resident = pl.resident;
   }
   return TSF_OK;
 }
@@ -449,40 +508,64 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
   k_sq<<<grid_for(n / 2), 256, 0, st>>>(reinterpret_cast<double *>(h->ws + pl.off_sq_p), pl.L1p, pl.C, pl.npp, n, 2.0);
   CKH(cudaGetLastError());
 
-  // per-instance host tables and inputs (copied; nothing is borrowed)
-  std::vector<double> tmp(static_cast<size_t>(std::max<int64_t>(n, 8))), permv(static_cast<size_t>(n));
-  std::vector<double> xs(static_cast<size_t>(n));
-  for (int32_t b = 0; b < B; ++b) {
-    const tsf_problem &q = p[b];
-    InstTables T;
-    inst_tables(q, &T);
-    double par[16] = {T.sigma, q.beta, 0.0, T.kappa, T.h, T.tau, 0.0, 0.0};
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_par), par, sizeof(par), cudaMemcpyHostToDevice));
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_lev), T.lev.data(), T.lev.size() * 8, cudaMemcpyHostToDevice));
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_hwc), T.hwc.data(), T.hwc.size() * 8, cudaMemcpyHostToDevice));
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_hwe), T.hwe.data(), T.hwe.size() * 8, cudaMemcpyHostToDevice));
-    // u^0 = phi(x_i)
-    if (q.phi) {
-      std::memcpy(tmp.data(), q.phi, size_t(n) * 8);
-    } else {
-      sample_points(q, xs.data(), nullptr);
-      for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = q.phi_fn(xs[size_t(i)], q.phi_ctx);
-    }
-    permute_host(n, pl.C, tmp.data(), permv.data());
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_vec + int64_t(V_U) * n * 8), permv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
-    CKH(cudaMemcpy(inst_ptr(h, b, pl.o_vec + int64_t(V_PHI) * n * 8), permv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
-    if (pl.src_kind == TSF_SRC_SEPARABLE) {
-      CKH(cudaMemcpy(inst_ptr(h, b, pl.o_scal), q.scal, size_t(M) * size_t(pl.K) * 8, cudaMemcpyHostToDevice));
-      for (int k = 0; k < pl.K; ++k) {
-        permute_host(n, pl.C, q.basis + int64_t(k) * n, permv.data());
-        CKH(cudaMemcpy(inst_ptr(h, b, pl.o_basis + int64_t(k) * n * 8), permv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+  // Per-instance inputs.  Every host-provided field of an instance block lies in [0, o_omega)
+  // (par, level tables, history weights, source, phi): they are written into ONE host image of
+  // B x o_omega bytes (permuted chunks where the kernels want them) and uploaded by a single
+  // pitched copy on the handle's stream, ordered after the zeroing memset above (pageable
+  // source: cudaMemcpy2DAsync returns once the image is staged, so it may be freed after).
+  // u^0 = phi is then set on the device by k_reset.  A device f table is borrowed (R-ftab).
+  {
+    const size_t img = size_t(pl.o_omega);
+    std::vector<char> himg(img * size_t(B), 0);
+    std::vector<double> tmp(static_cast<size_t>(std::max<int64_t>(n, 8))), xs(static_cast<size_t>(n));
+    std::vector<double> tl(static_cast<size_t>(M));
+    for (int32_t b = 0; b < B; ++b) {
+      const tsf_problem &q = p[b];
+      char *base = himg.data() + size_t(b) * img;
+      auto at = [&](int64_t off) { return reinterpret_cast<double *>(base + off); };
+      InstTables T;
+      inst_tables(q, &T);
+      double par[16] = {T.sigma, q.beta, 0.0, T.kappa, T.h, T.tau, 0.0, 0.0};
+      std::memcpy(at(pl.o_par), par, sizeof(par));
+      std::memcpy(at(pl.o_lev), T.lev.data(), T.lev.size() * 8);
+      std::memcpy(at(pl.o_hwc), T.hwc.data(), T.hwc.size() * 8);
+      std::memcpy(at(pl.o_hwe), T.hwe.data(), T.hwe.size() * 8);
+      sample_points(q, xs.data(), tl.data());
+      if (q.phi) {
+        std::memcpy(tmp.data(), q.phi, size_t(n) * 8);
+      } else {
+        for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = q.phi_fn(xs[size_t(i)], q.phi_ctx);
       }
-    } else if (pl.src_kind == TSF_SRC_TABLE) {
-      std::vector<double> ft(size_t(M) * size_t(n));
-      for (int64_t j = 0; j < M; ++j) permute_host(n, pl.C, q.f_table + j * n, ft.data() + j * n);
-      CKH(cudaMemcpy(inst_ptr(h, b, pl.o_ftab), ft.data(), ft.size() * 8, cudaMemcpyHostToDevice));
+      permute_host(n, pl.C, tmp.data(), at(pl.o_phi));
+      if (q.src_kind == TSF_SRC_SEPARABLE) {
+        std::memcpy(at(pl.o_scal), q.scal, size_t(M) * size_t(pl.K) * 8);
+        for (int k = 0; k < pl.K; ++k) permute_host(n, pl.C, q.basis + int64_t(k) * n, at(pl.o_basis) + int64_t(k) * n);
+      } else if (q.src_kind == TSF_SRC_TABLE && !pl.ftab_dev) {
+        for (int64_t j = 0; j < M; ++j) permute_host(n, pl.C, q.f_table + j * n, at(pl.o_ftab) + j * n);
+      } else if (q.src_kind == TSF_SRC_CALLBACK) {
+        // slow path: the host callback is evaluated once per level at
+        // t_{j+sigma} here, into the instance's source table (same kernel path as a table)
+        for (int64_t j = 0; j < M; ++j) {
+          q.f_cb(xs.data(), n, tl[size_t(j)], tmp.data(), q.f_ctx);
+          for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(tmp[size_t(i)])) {
+              set_error("f callback returned a non-finite value at level " + std::to_string(j));
+              return bail(TSF_E_ARG);
+            }
+          permute_host(n, pl.C, tmp.data(), at(pl.o_ftab) + j * n);
+        }
+      }
+    }
+    CKH(cudaMemcpy2DAsync(h->ws + pl.off_inst, pl.stride, himg.data(), img, img, size_t(B),
+                          cudaMemcpyHostToDevice, st));
+    if (pl.ftab_dev) {
+      std::vector<const double *> ptrs(static_cast<size_t>(B));
+      for (int32_t b = 0; b < B; ++b) ptrs[size_t(b)] = p[b].f_table;
+      CKH(cudaMemcpyAsync(h->ws + pl.off_fptr, ptrs.data(), size_t(B) * sizeof(double *), cudaMemcpyHostToDevice, st));
     }
   }
+  k_reset<<<grid_for((n + 4 * M) * B), 256, 0, st>>>(h->dp);     // u = phi, stats cleared
+  CKH(cudaGetLastError());
   // weights and one-time spectra (batched Stockham FFTs in the scratch region)
   k_weights<<<(B + 127) / 128, 128, 0, st>>>(dp);
   CKH(cudaGetLastError());
@@ -514,6 +597,20 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
     k_scatter_spec<<<grid_for(int64_t(nb) * (2 * n)), 256, 0, st>>>(dp, b0, nb, embS, preS);
     CKH(cudaGetLastError());
   }
+  if (pl.precond != TSF_NOPREC) {
+    k_prec_guard<<<unsigned(int64_t(B) * M), 256, 0, st>>>(dp);
+    CKH(cudaGetLastError());
+    std::vector<int32_t> stv(size_t(B) * size_t(M));
+    CKH(cudaMemcpy2DAsync(stv.data(), size_t(M) * 4, h->ws + pl.off_inst + pl.o_st, pl.stride, size_t(M) * 4,
+                          size_t(B), cudaMemcpyDeviceToHost, st));
+    CKH(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < stv.size(); ++k)
+      if (stv[k] == TSF_LEVEL_SINGULAR_PREC) {
+        set_error("preconditioner singular: |lambda_P| < 1e-14 max|lambda_P| (S:257) at instance " +
+                  std::to_string(k / size_t(M)) + ", level " + std::to_string(k % size_t(M)));
+        return bail(TSF_E_SINGULAR_PREC);
+      }
+  }
   CKH(cudaStreamSynchronize(st));
 
   // NEXT-2 setup: x = A^{-1} e_1, y = A^{-1} e_n by BiCGSTAB (eq3.4), then the spectra of the
@@ -541,10 +638,23 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
     CKH(cudaStreamSynchronize(st));
     for (int32_t b = 0; b < B; ++b) {
       double par[16];
-      CKH(cudaMemcpy(par, inst_ptr(h, b, pl.o_par), sizeof(par), cudaMemcpyDeviceToHost));
+      CKH(cudaMemcpyAsync(par, inst_ptr(h, b, pl.o_par), sizeof(par), cudaMemcpyDeviceToHost, st));
+      CKH(cudaStreamSynchronize(st));
       if (par[8] < 0 || par[9] < 0 || !std::isfinite(par[7])) {
         set_error("GSF setup (A x = e_1, A y = e_n) failed for instance " + std::to_string(b));
         return bail(TSF_E_BREAKDOWN);
+      }
+      // GSF applicability (eq. 3.5 "if xi_0 != 0"; |xi_0| < 1e-12 ||x||_inf is singular)
+      std::vector<double> xv(static_cast<size_t>(n));
+      CKH(cudaMemcpyAsync(xv.data(), inst_ptr(h, b, pl.o_vec + int64_t(V_GX) * n * 8), size_t(n) * 8,
+                          cudaMemcpyDeviceToHost, st));
+      CKH(cudaStreamSynchronize(st));
+      double xinf = 0.0;
+      for (double v : xv) xinf = std::max(xinf, std::fabs(v));
+      const double xi0 = 1.0 / par[7];
+      if (!(std::fabs(xi0) >= 1e-12 * xinf)) {
+        set_error("GSF inapplicable: |xi_0| < 1e-12 ||x||_inf (S:255) for instance " + std::to_string(b));
+        return bail(TSF_E_SINGULAR_PREC);
       }
     }
   }
@@ -591,7 +701,7 @@ int tsf_solve(tsf_handle *h) {
 int tsf_reset(tsf_handle *h) {
   if (!h) { set_error("null handle"); return TSF_E_ARG; }
   CK(cudaSetDevice(h->device));
-  k_reset<<<grid_for((h->pl.n + 3 * h->pl.M) * h->pl.B), 256, 0, h->st>>>(h->dp);
+  k_reset<<<grid_for((h->pl.n + 4 * h->pl.M) * h->pl.B), 256, 0, h->st>>>(h->dp);
   CK(cudaGetLastError());
   h->level = 0;
   return TSF_OK;
@@ -623,37 +733,61 @@ int tsf_sync(tsf_handle *h) {
   return rc;
 }
 
+// u^j of instances [b0, b0 + nb) -> out[nb][n] in natural order.  Host: one pitched D2H copy
+// of the permuted vectors on the handle's stream, then the host unpermute; device: a gather
+// kernel on the stream.  Synchronizes the stream.
+static int get_solutions_range(tsf_handle *h, int32_t b0, int32_t nb, double *out, int32_t out_on_device) {
+  CK(cudaSetDevice(h->device));
+  const int64_t n = h->pl.n;
+  const char *src = h->ws + h->pl.off_inst + size_t(b0) * h->pl.stride + size_t(h->pl.o_vec + int64_t(V_U) * n * 8);
+  if (out_on_device) {
+    k_gather_u<<<grid_for(int64_t(nb) * n), 256, 0, h->st>>>(h->dp, b0, nb, out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));
+    return TSF_OK;
+  }
+  std::vector<double> pv(size_t(nb) * size_t(n));
+  CK(cudaMemcpy2DAsync(pv.data(), size_t(n) * 8, src, h->pl.stride, size_t(n) * 8, size_t(nb),
+                       cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  for (int32_t b = 0; b < nb; ++b) unpermute_host(n, h->pl.C, pv.data() + size_t(b) * n, out + int64_t(b) * n);
+  return TSF_OK;
+}
+
 int tsf_get_solution(tsf_handle *h, int32_t inst, double *out, int32_t out_on_device) {
   if (!h || !out || inst < 0 || inst >= h->pl.B) { set_error("bad arguments"); return TSF_E_ARG; }
-  CK(cudaSetDevice(h->device));
-  CK(cudaStreamSynchronize(h->st));
-  const int64_t n = h->pl.n;
-  std::vector<double> pv(static_cast<size_t>(n)), nat(static_cast<size_t>(n));
-  CK(cudaMemcpy(pv.data(), inst_ptr(h, inst, h->pl.o_vec + int64_t(V_U) * n * 8), size_t(n) * 8, cudaMemcpyDeviceToHost));
-  unpermute_host(n, h->pl.C, pv.data(), nat.data());
-  if (out_on_device) CK(cudaMemcpy(out, nat.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
-  else std::memcpy(out, nat.data(), size_t(n) * 8);
-  return TSF_OK;
+  return get_solutions_range(h, inst, 1, out, out_on_device);
 }
 
 int tsf_get_solutions(tsf_handle *h, double *out, int32_t out_on_device) {
   if (!h || !out) { set_error("bad arguments"); return TSF_E_ARG; }
-  for (int32_t b = 0; b < h->pl.B; ++b) {
-    int rc = tsf_get_solution(h, b, out + int64_t(b) * h->pl.n, out_on_device);
-    if (rc) return rc;
-  }
+  return get_solutions_range(h, 0, h->pl.B, out, out_on_device);
+}
+
+static int get_rows(tsf_handle *h, int64_t off, size_t esz, void *dst) {
+  const size_t M = size_t(h->pl.M), B = size_t(h->pl.B);
+  CK(cudaMemcpy2DAsync(dst, M * esz, h->ws + h->pl.off_inst + off, h->pl.stride, M * esz, B,
+                       cudaMemcpyDeviceToHost, h->st));
   return TSF_OK;
 }
 
 int tsf_get_stats(tsf_handle *h, int32_t *iters_half, double *relres, int32_t *status) {
   if (!h) { set_error("null handle"); return TSF_E_ARG; }
   CK(cudaSetDevice(h->device));
+  int rc = TSF_OK;
+  if (iters_half && (rc = get_rows(h, h->pl.o_it, 4, iters_half))) return rc;
+  if (relres && (rc = get_rows(h, h->pl.o_rr, 8, relres))) return rc;
+  if (status && (rc = get_rows(h, h->pl.o_st, 4, status))) return rc;
   CK(cudaStreamSynchronize(h->st));
-  const size_t M = size_t(h->pl.M), B = size_t(h->pl.B);
-  const char *base = h->ws + h->pl.off_inst;
-  if (iters_half) CK(cudaMemcpy2D(iters_half, M * 4, base + h->pl.o_it, h->pl.stride, M * 4, B, cudaMemcpyDeviceToHost));
-  if (relres) CK(cudaMemcpy2D(relres, M * 8, base + h->pl.o_rr, h->pl.stride, M * 8, B, cudaMemcpyDeviceToHost));
-  if (status) CK(cudaMemcpy2D(status, M * 4, base + h->pl.o_st, h->pl.stride, M * 4, B, cudaMemcpyDeviceToHost));
+  return TSF_OK;
+}
+
+int tsf_get_true_residuals(tsf_handle *h, double *true_relres) {
+  if (!h || !true_relres) { set_error("bad arguments"); return TSF_E_ARG; }
+  CK(cudaSetDevice(h->device));
+  int rc = get_rows(h, h->pl.o_trr, 8, true_relres);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(h->st));
   return TSF_OK;
 }
 
@@ -665,12 +799,18 @@ int tsf_handle_info(const tsf_handle *h, tsf_plan_info *info) {
   info->embed_len = h->pl.n;
   info->precond_len = h->pl.n / 2;
   info->workspace_bytes = h->pl.total;
+  info->exchange = h->pl.C == 1 ? 0 : (h->pl.staged ? 1 : 2);
+  info->chunk = h->pl.chunk;
+  info->vsmem = h->pl.vsmem;
+  info->resident = h->pl.resident;
   return TSF_OK;
 }
 
 int tsf_destroy(tsf_handle *h) {
   if (!h) return TSF_OK;
   cudaSetDevice(h->device);
+  // the caller may free the workspace right after: let every enqueued launch finish first
+  cudaStreamSynchronize(h->st);
   if (h->step_exec) cudaGraphExecDestroy(h->step_exec);
   if (h->step_graph) cudaGraphDestroy(h->step_graph);
   delete h;
@@ -739,10 +879,10 @@ int tsf_debug_apply(tsf_handle *h, int32_t inst, int64_t j, int32_t which, const
   double *din = nullptr, *dout = nullptr;
   CK(cudaMalloc(&din, size_t(n) * 8));
   CK(cudaMalloc(&dout, size_t(n) * 8));
-  CK(cudaMemcpy(din, pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+  { CK(cudaMemcpyAsync(din, pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice, h->st)); CK(cudaStreamSynchronize(h->st)); }
   CK(launch_dbg_apply(h->pl, h->dp, inst, j, which, din, dout, h->st));
   CK(cudaStreamSynchronize(h->st));
-  CK(cudaMemcpy(po.data(), dout, size_t(n) * 8, cudaMemcpyDeviceToHost));
+  { CK(cudaMemcpyAsync(po.data(), dout, size_t(n) * 8, cudaMemcpyDeviceToHost, h->st)); CK(cudaStreamSynchronize(h->st)); }
   unpermute_host(n, h->pl.C, po.data(), y);
   cudaFree(din);
   cudaFree(dout);
@@ -761,7 +901,7 @@ int tsf_debug_apply_bench(tsf_handle *h, int32_t inst, int64_t j, int32_t reps, 
   double *din = nullptr, *dout = nullptr;
   CK(cudaMalloc(&din, size_t(n) * 8));
   CK(cudaMalloc(&dout, size_t(n) * 8));
-  CK(cudaMemcpy(din, x.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+  { CK(cudaMemcpyAsync(din, x.data(), size_t(n) * 8, cudaMemcpyHostToDevice, h->st)); CK(cudaStreamSynchronize(h->st)); }
   CK(launch_dbg_apply(h->pl, h->dp, inst, j, OP_A, din, dout, h->st, reps));   // warm-up
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -789,8 +929,8 @@ int tsf_debug_spectra(tsf_handle *h, int32_t inst, int64_t j, double *lamA, doub
   k_dbg_spectra<<<grid_for(2 * n), 256, 0, h->st>>>(h->dp, inst, j, dA, dP);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->st));
-  if (lamA) CK(cudaMemcpy(lamA, dA, size_t(n + 1) * 16, cudaMemcpyDeviceToHost));
-  if (lamP) CK(cudaMemcpy(lamP, dP, size_t(n / 2 + 1) * 16, cudaMemcpyDeviceToHost));
+  if (lamA) { CK(cudaMemcpyAsync(lamA, dA, size_t(n + 1) * 16, cudaMemcpyDeviceToHost, h->st)); CK(cudaStreamSynchronize(h->st)); }
+  if (lamP) { CK(cudaMemcpyAsync(lamP, dP, size_t(n / 2 + 1) * 16, cudaMemcpyDeviceToHost, h->st)); CK(cudaStreamSynchronize(h->st)); }
   cudaFree(dA);
   cudaFree(dP);
   return TSF_OK;
@@ -804,7 +944,7 @@ int tsf_debug_rhs(tsf_handle *h, int32_t inst, double *out) {
   CK(cudaStreamSynchronize(h->st));
   const int64_t n = h->pl.n;
   std::vector<double> pv(static_cast<size_t>(n));
-  CK(cudaMemcpy(pv.data(), inst_ptr(h, inst, h->pl.o_vec + int64_t(V_R) * n * 8), size_t(n) * 8, cudaMemcpyDeviceToHost));
+  { CK(cudaMemcpyAsync(pv.data(), inst_ptr(h, inst, h->pl.o_vec + int64_t(V_R) * n * 8), size_t(n) * 8, cudaMemcpyDeviceToHost, h->st)); CK(cudaStreamSynchronize(h->st)); }
   unpermute_host(n, h->pl.C, pv.data(), out);
   return TSF_OK;
 }
@@ -818,10 +958,10 @@ int tsf_debug_set_history(tsf_handle *h, int32_t inst, int64_t j, const double *
   for (int64_t s = 0; s < j; ++s) {
     for (int64_t i = 0; i < n; ++i) d[size_t(i)] = U[(s + 1) * n + i] - U[s * n + i];
     permute_host(n, h->pl.C, d.data(), pv.data());
-    CK(cudaMemcpy(inst_ptr(h, inst, h->pl.o_hist + s * n * 8), pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+    { CK(cudaMemcpyAsync(inst_ptr(h, inst, h->pl.o_hist + s * n * 8), pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice, h->st)); CK(cudaStreamSynchronize(h->st)); }
   }
   permute_host(n, h->pl.C, U + j * n, pv.data());
-  CK(cudaMemcpy(inst_ptr(h, inst, h->pl.o_vec + int64_t(V_U) * n * 8), pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice));
+  { CK(cudaMemcpyAsync(inst_ptr(h, inst, h->pl.o_vec + int64_t(V_U) * n * 8), pv.data(), size_t(n) * 8, cudaMemcpyHostToDevice, h->st)); CK(cudaStreamSynchronize(h->st)); }
   k_set_level<<<1, 32, 0, h->st>>>(h->dp.level, j);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->st));
@@ -830,6 +970,14 @@ int tsf_debug_set_history(tsf_handle *h, int32_t inst, int64_t j, const double *
 }
 
 }  // extern "C"
+
+extern "C" int tsf_debug_helper_state(tsf_handle *h, int64_t *out) {
+  if (!h || !out) { set_error("bad arguments"); return TSF_E_ARG; }
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(out, h->dp.sync, 8 * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return TSF_OK;
+}
 
 extern "C" int tsf_debug_prof(tsf_handle *h, uint64_t *out, int32_t reset) {
   if (!h || !out) { set_error("bad arguments"); return TSF_E_ARG; }

@@ -68,8 +68,10 @@ struct Inst {
   double2 *mul;          // per-level multiplier tables [n + n/2] (task order), HBM variant
   double2 *gsf;          // NEXT-2: spectra of the 4 triangular GSF factors [4][n+1] (task order)
   double2 *xg;           // unstaged clusters: L2 exchange buffer [C][L1e] of the local FFT outputs
+  const double *phi;     // u^0 (permuted chunks)
+  const double *fdev;    // borrowed device source table (natural order) or nullptr
   int32_t *it, *st;
-  double *rr;
+  double *rr, *trr;
 };
 
 __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
@@ -92,7 +94,10 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.xg = reinterpret_cast<double2 *>(base + P.o_xg);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
+  I.trr = reinterpret_cast<double *>(base + P.o_trr);
   I.st = reinterpret_cast<int32_t *>(base + P.o_st);
+  I.phi = reinterpret_cast<const double *>(base + P.o_phi);
+  I.fdev = P.ftab_dev ? P.fptr[b] : nullptr;
   return I;
 }
 
@@ -162,6 +167,17 @@ __device__ __forceinline__ int64_t ld_acquire(const int64_t *p) {
 __device__ __forceinline__ void st_release(int64_t *p, int64_t v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// History-helper handshake bounds: the solver waits at most
+// kHelperWaitNs for a pre-sum, helpers at most kHelperIdleNs for solver progress; on a timeout
+// the shared flag sync[5] is raised, helpers exit and the solver sums the history itself (same
+// summation order, same bits), so a launch that is only partly resident cannot deadlock.
+constexpr uint64_t kHelperWaitNs = 2000000;     // 2 ms
+constexpr uint64_t kHelperIdleNs = 200000000;   // 200 ms
 
 // Exchange state of one CTA: counts of operator exchanges and reductions so far (identical in
 // every thread of the cluster, since control flow is uniform); they select mbarrier phases.
@@ -189,6 +205,10 @@ struct Smem {
   double *wred, *cred;
   double *red;                       // push reductions: [2][16][4] CTA partials (double-buffered)
   uint64_t *mbar;                    // mbarriers: [0] exchange-in B, [1] exchange-back O, [2..3] red
+  int *flag;                         // CTA-wide broadcast word.  NOTE: the solve kernels declare NO
+                                     // static __shared__ variable: one would shift the dynamic buffers
+                                     // off their 128-byte alignment and break the bank-conflict-free
+                                     // swizzle (measured -9% at C3 for a single 4-byte static int)
   int fuse_min;                      // local FFTs of at least this length use radix-16 passes
   int chunk;                         // column pairs per chunk of the unstaged column stage (B = chunk buffer)
   unsigned long long *prof;
@@ -245,6 +265,7 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   s.cred = d + 40;
   s.red = d + 48;
   s.mbar = reinterpret_cast<uint64_t *>(d + 48 + 128);
+  s.flag = reinterpret_cast<int *>(d + 48 + 128 + 4);
   return s;
 }
 
@@ -1250,7 +1271,7 @@ __device__ __forceinline__ SpecOp make_gsf_op(const DevParams &P, const Inst &I,
 // Every vector loop visits element e = tid + q T, so each element is only ever touched by
 // the same thread and vector updates need no barrier.
 struct Vecs {
-  double2 *U, *X, *R, *RH, *P, *V, *S, *PH, *SH;
+  double2 *U, *X, *R, *RH, *P, *V, *S, *PH, *SH, *G;
 };
 
 // VS (compile time) = vectors in SMEM, so every vector access compiles to LDS/STS or LDG/STG
@@ -1263,10 +1284,10 @@ __device__ __forceinline__ Vecs vec_view(const DevParams &P, const Inst &I, cons
   if constexpr (VS) {
     double2 *b = sm.vs;
     v.U = b; v.X = b + npc; v.R = b + 2 * npc; v.RH = b + 3 * npc; v.P = b + 4 * npc;
-    v.V = b + 5 * npc; v.S = b + 6 * npc; v.PH = b + 7 * npc; v.SH = b + 8 * npc;
+    v.V = b + 5 * npc; v.S = b + 6 * npc; v.PH = b + 7 * npc; v.SH = b + 8 * npc; v.G = g(V_G);
   } else {
     v.U = g(V_U); v.X = g(V_X); v.R = g(V_R); v.RH = g(V_RH); v.P = g(V_P);
-    v.V = g(V_V); v.S = g(V_S); v.PH = g(V_PH); v.SH = g(V_SH);
+    v.V = g(V_V); v.S = g(V_S); v.PH = g(V_PH); v.SH = g(V_SH); v.G = g(V_G);
   }
   return v;
 }
@@ -1300,14 +1321,13 @@ struct T5 { double2 a, b, c, d, f; };
 
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
-// Returns the local partial ||g||^2; g is left in A[0..npc) (and A[npc..2npc) is zero).
-template <int C, bool STG>
-__device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
-                                            const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
-                                            double2 *Hsum, Xch &xs, bool use_pre = false) {
+// First half: the memory term into Hsum and u^j (zero-padded) into A; the caller applies B.
+template <int C>
+__device__ __forceinline__ void rhs_pre(const DevParams &P, const Smem &sm, const Inst &I, int64_t j, uint32_t r,
+                                        const double2 *U, double2 *Hsum, bool use_pre) {
+  // (use_pre is dropped below when the helpers do not deliver in time)
   const int npc = P.L1p;
   const int64_t n = P.n;
-  const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   TSF_PT0();
   const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
   const int64_t hstride = n / 2;  // double2 per history row
@@ -1317,11 +1337,24 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
   double2 *Hs = Hsum;
   if (use_pre) {
     // history pre-sum P^j = kappa (e_j d^0 + sum_{s=1}^{j-2} chat_{j-s} d^s) from the helper CTAs
-    // (computed during level j-1); add the newest row kappa chat_1 d^{j-1}
+    // (computed during level j-1); bounded wait, else this CTA sums its slice itself below
     if (threadIdx.x == 0) {
-      while (ld_acquire(P.sync + 1 + (j & 1)) != j) __nanosleep(64);
+      int ok = 0;
+      if (ld_acquire(P.sync + 5) == 0) {
+        const uint64_t t0 = gtimer_ns();
+        for (;;) {
+          if (ld_acquire(P.sync + 1 + (j & 1)) == j) { ok = 1; break; }
+          if (gtimer_ns() - t0 > kHelperWaitNs) { st_release(P.sync + 5, 1); break; }
+          __nanosleep(64);
+        }
+      }
+      *sm.flag = ok;
     }
     __syncthreads();
+    use_pre = *sm.flag != 0;
+    __syncthreads();              // the flag word is reused
+  }
+  if (use_pre) {
     const double2 *Pj = reinterpret_cast<const double2 *>(P.pre) + (j & 1) * hstride + r * npc;
     const double w1 = I.hwc[1];
     TSF_FOR_E(npc) { Hs[e] = caxpy(w1, H[(j - 1) * hstride + e], __ldcg(Pj + e)); }
@@ -1374,8 +1407,15 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
     sm.A[pidx(e)] = U[e];
     sm.A[pidx(e + npc)] = zero2();
   }
-  __syncthreads();
-  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs, I.xg);
+}
+
+// Second half of the RHS: g = Y - Hs + f from the product Y = B u^j; g into A[0..npc)
+// (A[npc..2npc) zero).  Returns the local partial ||g||^2.
+__device__ __forceinline__ double rhs_post(const DevParams &P, const Smem &sm, const Inst &I, int64_t j,
+                                           uint32_t r, const double2 *Y, const double2 *Hs) {
+  const int npc = P.L1p;
+  const int64_t n = P.n, hstride = n / 2;
+  const int C = P.C;
   double acc = 0.0;
   TSF_FOR_E(npc) {
     double2 g = Y[pidx(e)];
@@ -1384,14 +1424,31 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
       const double2 *Bs = reinterpret_cast<const double2 *>(I.basis) + r * npc;
       for (int k = 0; k < P.K; ++k) g = caxpy(I.scal[j * P.K + k], Bs[k * hstride + e], g);
     } else if (P.src_kind == TSF_SRC_TABLE) {
-      const double2 *F = reinterpret_cast<const double2 *>(I.ftab) + r * npc;
-      g = cadd(g, F[j * hstride + e]);
+      if (I.fdev) {          // borrowed natural-order table: packed value m = C e + r
+        const double2 *F = reinterpret_cast<const double2 *>(I.fdev + j * n);
+        g = cadd(g, __ldg(F + int64_t(e) * C + r));
+      } else {
+        const double2 *F = reinterpret_cast<const double2 *>(I.ftab) + r * npc;
+        g = cadd(g, F[j * hstride + e]);
+      }
     }
     sm.A[pidx(e)] = g;
     sm.A[pidx(e + npc)] = zero2();
     acc += cdot(g, g);
   }
   return acc;
+}
+
+// Whole RHS (debug hook): history, B u^j, g.
+template <int C, bool STG>
+__device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
+                                            const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
+                                            double2 *Hsum, Xch &xs) {
+  const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
+  rhs_pre<C>(P, sm, I, j, r, U, Hsum, false);
+  __syncthreads();
+  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs, I.xg);
+  return rhs_post(P, sm, I, j, r, Y, Hsum);
 }
 
 // ------------------------------------------------------------------------ one level
@@ -1468,6 +1525,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
   if (r == 0 && threadIdx.x == 0) {
     I.it[j] = 0;
     I.rr[j] = relres;
+    I.trr[j] = relres;
     I.st[j] = isfinite(relres) ? TSF_LEVEL_OK : TSF_LEVEL_DIVERGED;
   }
   __syncthreads();
@@ -1483,6 +1541,15 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
 // mode 0: level j of the scheme.  mode 1 / 2 (NEXT-2 setup, TSF_GSF): solve A x = e_1 / A y = e_n
 // (eq3.4) with the level-j operators and store the solution in V_GX / V_GY; no RHS,
 // history or statistics.
+//
+// Code shape: exactly two inlined operator applications per level, as measured fastest: the
+// Krylov loop's single site (every quarter step selects its operator) and one "cold" site shared
+// by the once-per-level products: S_RHS (B u^j), S_WARM (A u^j, warm start), S_TRUE
+// (A u^{j+1}, true residual).  Each inlined site adds the whole fused transform (~8k
+// instructions); a separate site per cold product, or an out-of-line copy, measured slower, and
+// a single state machine for everything cost ~6% at C3 against this shape.
+enum LevelState { S_RHS = 0, S_WARM = 1, S_TRUE = 2, S_KRYLOV = 3 };
+
 template <int C, int METHOD, bool STG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
                                             int64_t j, uint32_t r, Xch &xs, int mode = 0, int64_t j0 = 0) {
@@ -1491,19 +1558,26 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const bool prec = P.precond != TSF_NOPREC;
   const Geo ge = geo_embed(P, sm), gp = geo_prec(P, sm);
-  fill_mul(P, I, j, r, sm);      // visible after the first barrier of rhs_phase
+  fill_mul(P, I, j, r, sm);      // visible after the first barrier below
   const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
-  const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const SpecOp opP = make_op(P, I, j, OP_PINV, r, sm);
   double2 *__restrict__ X = V.X, *__restrict__ R = V.R, *__restrict__ RH = V.RH, *__restrict__ PV = V.P;
   double2 *__restrict__ VV = V.V, *__restrict__ S = V.S, *__restrict__ PH = V.PH, *__restrict__ SH = V.SH;
+  double2 *__restrict__ G = V.G;
 #ifdef TSF_PROFILE
   const long long tlev0 = clock64();
 #endif
+  const bool warm = P.x0_warm && mode == 0;
+  const bool tres = P.true_res && mode == 0;
+  int hs = 0, status = TSF_LEVEL_OK;
+  double relres = 0.0, gg = 0.0, rr0 = 0.0;
+  const double2 *Y = sm.A;       // output buffer of the last operator application
 
   double g2[1] = {0.0};
+  int ph;
   if (mode == 0) {
-    g2[0] = rhs_phase<C, STG>(P, sm, I, ge, opB, j, r, V.U, V.X, xs, P.helpers > 0 && j >= 2 && j >= j0 + 1);
+    rhs_pre<C>(P, sm, I, j, r, V.U, V.X, P.helpers > 0 && j >= 2 && j >= j0 + 1);
+    ph = S_RHS;
   } else {
     // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
     const int64_t m = mode == 1 ? 0 : n / 2 - 1;
@@ -1512,293 +1586,355 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       const double2 g = hit ? (mode == 1 ? make_double2(1.0, 0.0) : make_double2(0.0, 1.0)) : zero2();
       sm.A[pidx(e)] = g;
       sm.A[pidx(e + npc)] = zero2();
+      R[e] = g;
+      G[e] = g;
+      if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
+      if (METHOD == TSF_PCGS) RH[e] = g;
+      X[e] = zero2();
       g2[0] += cdot(g, g);
     }
+    csum<C, 1>(g2, sm, xs);
+    gg = rr0 = g2[0];
+    ph = S_KRYLOV;
   }
-  if constexpr (METHOD == TSF_GSF) {
-    if (mode == 0 && j >= 1) {
-      gsf_level<C, STG>(P, I, sm, V, j, r, xs, g2[0]);
-      return;
-    }
-  }
-  TSF_FOR_E(npc) {
-    const double2 g = sm.A[pidx(e)];
-    R[e] = g;
-    if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
-    if (METHOD == TSF_PCGS) RH[e] = g;
-    X[e] = zero2();
-  }
-  csum<C, 1>(g2, sm, xs);
-  const double rr0 = g2[0];
-  const double rn0 = sqrt(rr0);
-  int hs = 0, status = TSF_LEVEL_OK;
-  double relres = 0.0;
-  const double2 *Y = sm.A;      // output buffer of the last operator application
 
-  if (rr0 > 0.0 && (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF)) {
-    // One BiCGSTAB iteration = four operator applications, h = 0..3: phat = P^{-1} p,
-    // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
-    // and geometry are selected per h) so the hot loop's code stays small for the instruction
-    // cache; the vector work before/after each application is dispatched on h.
-    double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
-    TSF_FOR_E(npc) { sm.A[pidx(e)] = R[e]; }     // p_0 = r_0
-    bool done = false;
-    for (int h = 0; !done; h = (h + 1) & 3) {
-      const bool isP = !(h & 1);
-      if (isP && !prec) {
-        Y = sm.A;
-      } else {
+  for (;;) {
+    if (ph != S_KRYLOV) {
+      // ---- the cold application site: B u^j, A u^j (warm start) or A u^{j+1} (true residual)
+      {
+        const SpecOp op = ph == S_RHS ? make_op(P, I, j, OP_B, r, sm) : opA;
         __syncthreads();
-        const SpecOp op = isP ? opP : opA;
-        const Geo g = isP ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
+        Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
       }
-      if (isP) {
-        // h = 0: phat = Y; h = 2: shat = Y.  Either becomes the (padded) input of A.
-        double2 *const Dst = h == 0 ? PH : SH;
+      if (ph == S_TRUE) {
+        // true residual at exit (SURVEY reading c13): ||g - A u^{j+1}|| / ||g||
+        double tr[1] = {0.0};
         TSF_FOR_E(npc) {
-          const double2 z = Y[pidx(e)];
-          Dst[e] = z;
-          sm.A[pidx(e)] = z;
+          const double2 d = csub(G[e], Y[pidx(e)]);
+          tr[0] += cdot(d, d);
+        }
+        csum<C, 1>(tr, sm, xs);
+        if (r == 0 && threadIdx.x == 0) I.trr[j] = gg > 0.0 ? sqrt(tr[0] / gg) : 0.0;
+        break;
+      }
+      if (ph == S_RHS) {
+        g2[0] = rhs_post(P, sm, I, j, r, Y, V.X);
+        if constexpr (METHOD == TSF_GSF) {
+          if (j >= 1) {          // NEXT-2: the level by the Gohberg-Semencul formula
+            gsf_level<C, STG>(P, I, sm, V, j, r, xs, g2[0]);
+            return;
+          }
+        }
+        if (warm) {
+          // NEXT-3 warm start x0 = u^j: r0 = g - A u^j, stop on ||r|| < tol ||g||
+          TSF_FOR_E(npc) {
+            G[e] = sm.A[pidx(e)];
+            sm.A[pidx(e)] = V.U[e];
+            sm.A[pidx(e + npc)] = zero2();
+          }
+          ph = S_WARM;
+          continue;
+        }
+        TSF_FOR_E(npc) {
+          const double2 g = sm.A[pidx(e)];
+          R[e] = g;
+          G[e] = g;
+          if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
+          if (METHOD == TSF_PCGS) RH[e] = g;
+          X[e] = zero2();
+        }
+        csum<C, 1>(g2, sm, xs);
+        gg = rr0 = g2[0];
+      } else {                   // S_WARM
+        double w2[2] = {g2[0], 0.0};
+        TSF_FOR_E(npc) {
+          const double2 r0 = csub(G[e], Y[pidx(e)]);
+          R[e] = r0;
+          if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = r0; PV[e] = r0; }
+          if (METHOD == TSF_PCGS) RH[e] = r0;
+          X[e] = V.U[e];
+          w2[1] += cdot(r0, r0);
+        }
+        __syncthreads();         // Y may alias A
+        TSF_FOR_E(npc) {
+          sm.A[pidx(e)] = R[e];
           sm.A[pidx(e + npc)] = zero2();
         }
-        continue;
-      }
-      if (h == 1) {
-        // v = Y; alpha = rho / (r^.v); s = r - alpha v; half-step exit on ||s||
-        double d[1] = {0.0};
-        batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = RH[e]; }, [&](int e, T1 &t) {
-          const double2 v = Y[pidx(e)];
-          VV[e] = v;
-          d[0] += cdot(t.a, v);
-        });
-        csum<C, 1>(d, sm, xs);
-        if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-        alpha = rho / d[0];
-        double ss[1] = {0.0};
-        batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = VV[e]; t.b = R[e]; }, [&](int e, T2 &t) {
-          const double2 s = caxpy(-alpha, t.a, t.b);
-          S[e] = s;
-          sm.A[pidx(e)] = s;
-          ss[0] += cdot(s, s);
-        });
-        csum<C, 1>(ss, sm, xs);
-        if (sqrt(ss[0]) < P.tol * rn0) {
-          batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = PH[e]; t.b = X[e]; },
-                                 [&](int e, T2 &t) { X[e] = caxpy(alpha, t.a, t.b); });
-          hs += 1;
-          relres = sqrt(ss[0]) / rn0;
-          break;
-        }
-        continue;
-      }
-      // h == 3: t = Y; omega = t.s / t.t; x += alpha phat + omega shat; r = s - omega t
-      double tt[2] = {0.0, 0.0};
-      batched<TSF_BATCH, T1>(npc, [&](int e, T1 &t) { t.a = S[e]; }, [&](int e, T1 &ts) {
-        const double2 t = Y[pidx(e)];
-        tt[0] += cdot(t, ts.a);
-        tt[1] += cdot(t, t);
-      });
-      csum<C, 2>(tt, sm, xs);
-      if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      omega = tt[0] / tt[1];
-      double rr[2] = {0.0, 0.0};
-      batched<(TSF_BATCH > 2 ? 2 : TSF_BATCH), T5>(npc, [&](int e, T5 &t) { t.a = X[e]; t.b = SH[e]; t.c = PH[e]; t.d = S[e]; t.f = RH[e]; },
-                     [&](int e, T5 &t) {
-                       X[e] = caxpy(omega, t.b, caxpy(alpha, t.c, t.a));
-                       const double2 rn = caxpy(-omega, Y[pidx(e)], t.d);
-                       R[e] = rn;
-                       rr[0] += cdot(t.f, rn);
-                       rr[1] += cdot(rn, rn);
-                     });
-      csum<C, 2>(rr, sm, xs);
-      hs += 2;
-      relres = sqrt(rr[1]) / rn0;
-      if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
-      if (relres < P.tol) break;
-      if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
-      if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      beta = (rr[0] / rho) * (alpha / omega);
-      rho = rr[0];
-      // next p = r + beta (p - omega v) into A
-      batched<TSF_BATCH, T3>(npc, [&](int e, T3 &t) { t.a = R[e]; t.b = VV[e]; t.c = PV[e]; },
-                             [&](int e, T3 &t) {
-                               const double2 pv = caxpy(beta, caxpy(-omega, t.b, t.c), t.a);
-                               PV[e] = pv;
-                               sm.A[pidx(e)] = pv;
-                             });
-    }
-  } else if (rr0 > 0.0 && METHOD == TSF_PCGS) {
-    // Preconditioned CGS (the paper's PCGS; MATLAB pcgs), right-preconditioned:
-    // shadow rt = r0, u = r + beta q, p = u + beta (q + beta p), phat = P^{-1} p, vhat = A phat,
-    // alpha = rho / (rt.vhat), q = u - alpha vhat, uhat = P^{-1}(u + q), x += alpha uhat,
-    // r -= alpha A uhat.  Vector slots: u -> S, p -> PV, q -> VV, phat -> PH.  As for BiCGSTAB,
-    // the four applications of an iteration (h = 0..3: P^{-1}, A, P^{-1}, A) share one inlined
-    // apply.
-    double rho = rr0, alpha = 0.0;
-    TSF_FOR_E(npc) {                           // u_0 = p_0 = r_0
-      const double2 rv = R[e];
-      S[e] = rv;
-      PV[e] = rv;
-      sm.A[pidx(e)] = rv;
-    }
-    for (int h = 0;; h = (h + 1) & 3) {
-      const bool isP = !(h & 1);
-      if (isP && !prec) {
-        Y = sm.A;
-      } else {
-        __syncthreads();
-        const SpecOp op = isP ? opP : opA;
-        const Geo g = isP ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
-      }
-      if (h == 0) {                            // phat
-        TSF_FOR_E(npc) {
-          const double2 ph = Y[pidx(e)];
-          PH[e] = ph;
-          sm.A[pidx(e)] = ph;
-          sm.A[pidx(e + npc)] = zero2();
-        }
-        continue;
-      }
-      if (h == 1) {                            // vhat: alpha, q = u - alpha vhat, A <- u + q
-        double sg[1] = {0.0};
-        TSF_FOR_E(npc) { sg[0] += cdot(RH[e], Y[pidx(e)]); }
-        csum<C, 1>(sg, sm, xs);
-        if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-        alpha = rho / sg[0];
-        TSF_FOR_E(npc) {                       // Y may alias A: read before the write
-          const double2 u = S[e];
-          const double2 q = caxpy(-alpha, Y[pidx(e)], u);
-          VV[e] = q;
-          sm.A[pidx(e)] = cadd(u, q);
-        }
-        continue;
-      }
-      if (h == 2) {                            // uhat: x += alpha uhat, A <- uhat
-        TSF_FOR_E(npc) {
-          const double2 uh = Y[pidx(e)];
-          X[e] = caxpy(alpha, uh, X[e]);
-          sm.A[pidx(e)] = uh;
-          sm.A[pidx(e + npc)] = zero2();
-        }
-        continue;
-      }
-      // h == 3: A uhat: r -= alpha A uhat; rho' = rt.r; ||r||
-      double rr[2] = {0.0, 0.0};
-      TSF_FOR_E(npc) {
-        const double2 rn = caxpy(-alpha, Y[pidx(e)], R[e]);
-        R[e] = rn;
-        rr[0] += cdot(RH[e], rn);
-        rr[1] += cdot(rn, rn);
-      }
-      csum<C, 2>(rr, sm, xs);
-      hs += 2;
-      relres = sqrt(rr[1]) / rn0;
-      if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
-      if (relres < P.tol) break;
-      if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
-      if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      const double beta = rr[0] / rho;
-      rho = rr[0];
-      TSF_FOR_E(npc) {                         // u = r + beta q; p = u + beta (q + beta p)
-        const double2 q = VV[e];
-        const double2 u = caxpy(beta, q, R[e]);
-        const double2 pv = caxpy(beta, caxpy(beta, PV[e], q), u);
-        S[e] = u;
-        PV[e] = pv;
-        sm.A[pidx(e)] = pv;
+        csum<C, 2>(w2, sm, xs);
+        gg = w2[0];
+        rr0 = w2[1];
       }
     }
-  } else if (rr0 > 0.0 && METHOD == TSF_CGNR) {
-    // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r = P^{-T} A^T r, p = z;
-    // per iteration phat = P^{-1} p, q = A phat, a = gamma/||q||^2, x += a phat, r -= a q,
-    // z = P^{-T} A^T r, beta = ||z||^2 / gamma, p = z + beta p.  The four applications
-    // (h = 2: A^T, 3: P^{-T}, 0: P^{-1}, 1: A) share one inlined apply; the loop enters at h = 2
-    // with r = g already in A (rhs_phase).
-    const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
-    const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
-    double gam = 0.0, a = 0.0;
-    bool first = true;
-    for (int h = 2;; h = (h + 1) & 3) {
-      const bool isP = !(h & 1);                // h = 0: P^{-1}, h = 2: A^T
-      const bool isPre = h == 0 || h == 3;
-      if (isPre && !prec) {
-        Y = sm.A;
-      } else {
-        __syncthreads();
-        const SpecOp op = h == 0 ? opP : (h == 1 ? opA : (h == 2 ? opAT : opPT));
-        const Geo g = isPre ? gp : ge;
-        Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
-      }
-      (void)isP;
-      if (h == 2) {                            // A^T r -> first npc values into A for P^{-T}
-        TSF_FOR_E(npc) {
-          const double2 v = Y[pidx(e)];
-          sm.A[pidx(e)] = v;
+    // ---- Krylov solve from r_0 (in R and A), ||r_0||^2 = rr0, stop on ||r|| < tol ||g||
+    const double rn0 = sqrt(gg);
+    relres = rn0 > 0.0 ? sqrt(rr0) / rn0 : 0.0;
+    const bool iterate = rr0 > 0.0 && !(warm && sqrt(rr0) < P.tol * rn0);
+
+    if (iterate && (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF)) {
+      // One BiCGSTAB iteration = four operator applications, h = 0..3: phat = P^{-1} p,
+      // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
+      // and geometry are selected per h) so the hot loop's code stays small for the instruction
+      // cache; the vector work before/after each application is dispatched on h.
+      double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
+      for (int h = 0;; h = (h + 1) & 3) {
+        const bool isP = !(h & 1);
+        if (isP && !prec) {
+          Y = sm.A;
+        } else {
+          __syncthreads();
+          const SpecOp op = isP ? opP : opA;
+          const Geo g = isP ? gp : ge;
+          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
         }
-        continue;
-      }
-      if (h == 3) {                            // z = P^{-T} A^T r; gamma, beta; p = z + beta p
-        double zz[1] = {0.0};
-        TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
-        csum<C, 1>(zz, sm, xs);
-        const double beta = first ? 0.0 : zz[0] / gam;
-        gam = zz[0];
+        if (isP) {
+          // h = 0: phat = Y; h = 2: shat = Y.  Either becomes the (padded) input of A.
+          double2 *const Dst = h == 0 ? PH : SH;
+          TSF_FOR_E(npc) {
+            const double2 z = Y[pidx(e)];
+            Dst[e] = z;
+            sm.A[pidx(e)] = z;
+            sm.A[pidx(e + npc)] = zero2();
+          }
+          continue;
+        }
+        if (h == 1) {
+          // v = Y; alpha = rho / (r^.v); s = r - alpha v; half-step exit on ||s||
+          double d[1] = {0.0};
+          TSF_FOR_E(npc) {
+            const double2 v = Y[pidx(e)];
+            VV[e] = v;
+            d[0] += cdot(RH[e], v);
+          }
+          csum<C, 1>(d, sm, xs);
+          if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+          alpha = rho / d[0];
+          double ss[1] = {0.0};
+          TSF_FOR_E(npc) {
+            const double2 sv = caxpy(-alpha, VV[e], R[e]);
+            S[e] = sv;
+            sm.A[pidx(e)] = sv;
+            ss[0] += cdot(sv, sv);
+          }
+          csum<C, 1>(ss, sm, xs);
+          if (sqrt(ss[0]) < P.tol * rn0) {
+            TSF_FOR_E(npc) { X[e] = caxpy(alpha, PH[e], X[e]); }
+            hs += 1;
+            relres = sqrt(ss[0]) / rn0;
+            break;
+          }
+          continue;
+        }
+        // h == 3: t = Y; omega = t.s / t.t; x += alpha phat + omega shat; r = s - omega t
+        double tt[2] = {0.0, 0.0};
         TSF_FOR_E(npc) {
-          const double2 z = Y[pidx(e)];
-          const double2 pv = first ? z : caxpy(beta, PV[e], z);
+          const double2 t = Y[pidx(e)];
+          const double2 sv = S[e];
+          tt[0] += cdot(t, sv);
+          tt[1] += cdot(t, t);
+        }
+        csum<C, 2>(tt, sm, xs);
+        if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        omega = tt[0] / tt[1];
+        double rr[2] = {0.0, 0.0};
+        TSF_FOR_E(npc) {
+          X[e] = caxpy(omega, SH[e], caxpy(alpha, PH[e], X[e]));
+          const double2 rn = caxpy(-omega, Y[pidx(e)], S[e]);
+          R[e] = rn;
+          rr[0] += cdot(RH[e], rn);
+          rr[1] += cdot(rn, rn);
+        }
+        csum<C, 2>(rr, sm, xs);
+        hs += 2;
+        relres = sqrt(rr[1]) / rn0;
+        if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+        if (relres < P.tol) break;
+        if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
+        if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        beta = (rr[0] / rho) * (alpha / omega);
+        rho = rr[0];
+        // next p = r + beta (p - omega v) into A
+        TSF_FOR_E(npc) {
+          const double2 pv = caxpy(beta, caxpy(-omega, VV[e], PV[e]), R[e]);
           PV[e] = pv;
           sm.A[pidx(e)] = pv;
         }
-        first = false;
-        continue;
       }
-      if (h == 0) {                            // phat
-        TSF_FOR_E(npc) {
-          const double2 ph = Y[pidx(e)];
-          PH[e] = ph;
-          sm.A[pidx(e)] = ph;
-          sm.A[pidx(e + npc)] = zero2();
+    } else if (iterate && METHOD == TSF_PCGS) {
+      // Preconditioned CGS (the paper's PCGS; MATLAB pcgs), right-preconditioned:
+      // shadow rt = r0, u = r + beta q, p = u + beta (q + beta p), phat = P^{-1} p, vhat = A phat,
+      // alpha = rho / (rt.vhat), q = u - alpha vhat, uhat = P^{-1}(u + q), x += alpha uhat,
+      // r -= alpha A uhat.  Vector slots: u -> S, p -> PV, q -> VV, phat -> PH.  As for BiCGSTAB,
+      // the four applications of an iteration (h = 0..3: P^{-1}, A, P^{-1}, A) share one inlined
+      // apply.
+      double rho = rr0, alpha = 0.0;
+      TSF_FOR_E(npc) {                           // u_0 = p_0 = r_0
+        const double2 rv = R[e];
+        S[e] = rv;
+        PV[e] = rv;
+      }
+      for (int h = 0;; h = (h + 1) & 3) {
+        const bool isP = !(h & 1);
+        if (isP && !prec) {
+          Y = sm.A;
+        } else {
+          __syncthreads();
+          const SpecOp op = isP ? opP : opA;
+          const Geo g = isP ? gp : ge;
+          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
         }
-        continue;
+        if (h == 0) {                            // phat
+          TSF_FOR_E(npc) {
+            const double2 phv = Y[pidx(e)];
+            PH[e] = phv;
+            sm.A[pidx(e)] = phv;
+            sm.A[pidx(e + npc)] = zero2();
+          }
+          continue;
+        }
+        if (h == 1) {                            // vhat: alpha, q = u - alpha vhat, A <- u + q
+          double sg[1] = {0.0};
+          TSF_FOR_E(npc) { sg[0] += cdot(RH[e], Y[pidx(e)]); }
+          csum<C, 1>(sg, sm, xs);
+          if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+          alpha = rho / sg[0];
+          TSF_FOR_E(npc) {                       // Y may alias A: read before the write
+            const double2 u = S[e];
+            const double2 q = caxpy(-alpha, Y[pidx(e)], u);
+            VV[e] = q;
+            sm.A[pidx(e)] = cadd(u, q);
+          }
+          continue;
+        }
+        if (h == 2) {                            // uhat: x += alpha uhat, A <- uhat
+          TSF_FOR_E(npc) {
+            const double2 uh = Y[pidx(e)];
+            X[e] = caxpy(alpha, uh, X[e]);
+            sm.A[pidx(e)] = uh;
+            sm.A[pidx(e + npc)] = zero2();
+          }
+          continue;
+        }
+        // h == 3: A uhat: r -= alpha A uhat; rho' = rt.r; ||r||
+        double rr[2] = {0.0, 0.0};
+        TSF_FOR_E(npc) {
+          const double2 rn = caxpy(-alpha, Y[pidx(e)], R[e]);
+          R[e] = rn;
+          rr[0] += cdot(RH[e], rn);
+          rr[1] += cdot(rn, rn);
+        }
+        csum<C, 2>(rr, sm, xs);
+        hs += 2;
+        relres = sqrt(rr[1]) / rn0;
+        if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+        if (relres < P.tol) break;
+        if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
+        if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        const double beta = rr[0] / rho;
+        rho = rr[0];
+        TSF_FOR_E(npc) {                         // u = r + beta q; p = u + beta (q + beta p)
+          const double2 q = VV[e];
+          const double2 u = caxpy(beta, q, R[e]);
+          const double2 pv = caxpy(beta, caxpy(beta, PV[e], q), u);
+          S[e] = u;
+          PV[e] = pv;
+          sm.A[pidx(e)] = pv;
+        }
       }
-      // h == 1: q = A phat; a = gamma / ||q||^2; x += a phat; r -= a q; ||r||
-      double qq[1] = {0.0};
-      TSF_FOR_E(npc) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
-      csum<C, 1>(qq, sm, xs);
-      if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
-      a = gam / qq[0];
-      double rl[1] = {0.0};
-      TSF_FOR_E(npc) {
-        X[e] = caxpy(a, PH[e], X[e]);
-        const double2 rn = caxpy(-a, Y[pidx(e)], R[e]);
-        R[e] = rn;
-        sm.A[pidx(e)] = rn;
-        sm.A[pidx(e + npc)] = zero2();
-        rl[0] += cdot(rn, rn);
+    } else if (iterate && METHOD == TSF_CGNR) {
+      // CGLS on K = A P^{-1} (DESIGN.md R-cgnr): y0 = 0, r = b, z = K^T r = P^{-T} A^T r, p = z;
+      // per iteration phat = P^{-1} p, q = A phat, a = gamma/||q||^2, x += a phat, r -= a q,
+      // z = P^{-T} A^T r, beta = ||z||^2 / gamma, p = z + beta p.  The four applications
+      // (h = 2: A^T, 3: P^{-T}, 0: P^{-1}, 1: A) share one inlined apply; the loop enters at h = 2
+      // with r already in A.
+      const SpecOp opAT = make_op(P, I, j, OP_AT, r, sm);
+      const SpecOp opPT = make_op(P, I, j, OP_PTINV, r, sm);
+      double gam = 0.0, a = 0.0;
+      bool first = true;
+      for (int h = 2;; h = (h + 1) & 3) {
+        const bool isPre = h == 0 || h == 3;
+        if (isPre && !prec) {
+          Y = sm.A;
+        } else {
+          __syncthreads();
+          const SpecOp op = h == 0 ? opP : (h == 1 ? opA : (h == 2 ? opAT : opPT));
+          const Geo g = isPre ? gp : ge;
+          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
+        }
+        if (h == 2) {                            // A^T r -> first npc values into A for P^{-T}
+          TSF_FOR_E(npc) { sm.A[pidx(e)] = Y[pidx(e)]; }
+          continue;
+        }
+        if (h == 3) {                            // z = P^{-T} A^T r; gamma, beta; p = z + beta p
+          double zz[1] = {0.0};
+          TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+          csum<C, 1>(zz, sm, xs);
+          const double beta = first ? 0.0 : zz[0] / gam;
+          gam = zz[0];
+          TSF_FOR_E(npc) {
+            const double2 z = Y[pidx(e)];
+            const double2 pv = first ? z : caxpy(beta, PV[e], z);
+            PV[e] = pv;
+            sm.A[pidx(e)] = pv;
+          }
+          first = false;
+          continue;
+        }
+        if (h == 0) {                            // phat
+          TSF_FOR_E(npc) {
+            const double2 phv = Y[pidx(e)];
+            PH[e] = phv;
+            sm.A[pidx(e)] = phv;
+            sm.A[pidx(e + npc)] = zero2();
+          }
+          continue;
+        }
+        // h == 1: q = A phat; a = gamma / ||q||^2; x += a phat; r -= a q; ||r||
+        double qq[1] = {0.0};
+        TSF_FOR_E(npc) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+        csum<C, 1>(qq, sm, xs);
+        if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+        a = gam / qq[0];
+        double rl[1] = {0.0};
+        TSF_FOR_E(npc) {
+          X[e] = caxpy(a, PH[e], X[e]);
+          const double2 rn = caxpy(-a, Y[pidx(e)], R[e]);
+          R[e] = rn;
+          sm.A[pidx(e)] = rn;
+          sm.A[pidx(e + npc)] = zero2();
+          rl[0] += cdot(rn, rn);
+        }
+        csum<C, 1>(rl, sm, xs);
+        hs += 2;
+        relres = sqrt(rl[0] / gg);
+        if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+        if (relres < P.tol) break;
+        if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
       }
-      csum<C, 1>(rl, sm, xs);
-      hs += 2;
-      relres = sqrt(rl[0] / rr0);
-      if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
-      if (relres < P.tol) break;
-      if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
     }
+    if (!tres) break;
+    // true residual next, through the cold site: A <- x
+    __syncthreads();             // every thread done with the last Y
+    TSF_FOR_E(npc) {
+      sm.A[pidx(e)] = X[e];
+      sm.A[pidx(e + npc)] = zero2();
+    }
+    ph = S_TRUE;
   }
+
   if (mode != 0) {               // GSF setup: keep the solution of eq3.4
-    double2 *G = reinterpret_cast<double2 *>(I.vec + (mode == 1 ? V_GX : V_GY) * n) + r * npc;
-    TSF_FOR_E(npc) { G[e] = X[e]; }
+    double2 *Gx = reinterpret_cast<double2 *>(I.vec + (mode == 1 ? V_GX : V_GY) * n) + r * npc;
+    TSF_FOR_E(npc) { Gx[e] = X[e]; }
     if (r == 0 && threadIdx.x == 0) I.par[mode == 1 ? 8 : 9] = double(status == TSF_LEVEL_OK ? hs : -1 - status);
     __syncthreads();
     return;
   }
   // finalize (alg1 step 3 result): d^j = u^{j+1} - u^j, u^j <- u^{j+1}
   double2 *Hj = reinterpret_cast<double2 *>(I.hist + j * n) + r * npc;
-  batched<TSF_BATCH, T2>(npc, [&](int e, T2 &t) { t.a = X[e]; t.b = V.U[e]; }, [&](int e, T2 &t) {
-    Hj[e] = csub(t.a, t.b);
-    V.U[e] = t.a;
-  });
+  TSF_FOR_E(npc) {
+    const double2 x = X[e], u = V.U[e];
+    Hj[e] = csub(x, u);
+    V.U[e] = x;
+  }
   if (r == 0 && threadIdx.x == 0) {
     I.it[j] = hs;
     I.rr[j] = relres;
@@ -1827,7 +1963,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 // fence + atomic); helpers wait for C (J - 1 - j0) of them, write their slice, count themselves
 // in sync[3 + (J & 1)], and the last one publishes ready[J & 1] = J (release store).
 template <int C>
-__device__ void hist_helper(const DevParams &P, int32_t nlev) {
+__device__ void hist_helper(const DevParams &P, int32_t nlev, int *quit) {
   const Inst I = inst_view(P, 0);
   const int h = int(blockIdx.x) - P.B * C, nh = P.helpers;
   const int64_t n = P.n, half = n / 2;
@@ -1835,8 +1971,23 @@ __device__ void hist_helper(const DevParams &P, int32_t nlev) {
   const double2 *Hd = reinterpret_cast<const double2 *>(I.hist);
   for (int64_t J = (j0 + 1 > 2 ? j0 + 1 : 2); J < jend; ++J) {
     if (threadIdx.x == 0) {
-      while (ld_acquire(P.sync) < int64_t(C) * (J - 1 - j0)) __nanosleep(256);
+      // wait for the solver to finish level J-2 (its CTAs count levels in sync[0]); give up when
+      // it makes no progress for kHelperIdleNs or the solver stopped relying on the helpers
+      int q = 0;
+      int64_t last = -1;
+      uint64_t t0 = gtimer_ns();
+      for (;;) {
+        if (ld_acquire(P.sync + 5) != 0) { q = 1; break; }
+        const int64_t v = ld_acquire(P.sync);
+        if (v >= int64_t(C) * (J - 1 - j0)) break;
+        if (v != last) { last = v; t0 = gtimer_ns(); }
+        else if (gtimer_ns() - t0 > kHelperIdleNs) { st_release(P.sync + 5, 1); q = 1; break; }
+        __nanosleep(256);
+      }
+      *quit = q;
     }
+    __syncthreads();
+    if (*quit) return;
     __syncthreads();
     double2 *Pj = reinterpret_cast<double2 *>(P.pre) + (J & 1) * half;
     const double wJ = I.hwe[J];
@@ -1877,9 +2028,9 @@ __device__ void hist_helper(const DevParams &P, int32_t nlev) {
 template <int C, int METHOD, bool STG, bool VS>
 __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
     k_solve(DevParams P, int32_t nlev, int32_t mode) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   if (int(blockIdx.x) >= P.B * C) {   // history-helper clusters (single-instance launches)
-    if constexpr (C > 1) hist_helper<C>(P, nlev);
+    if constexpr (C > 1) hist_helper<C>(P, nlev, reinterpret_cast<int *>(smem_raw));
     return;
   }
   const int b = blockIdx.x / C;
@@ -1925,7 +2076,7 @@ __global__ void k_advance(int64_t *level, int64_t by, int64_t M);
 template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t reps, int b, int64_t j,
                                                               int which, const double *in, double *out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
 #ifdef TSF_PROFILE
@@ -1972,7 +2123,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
 // Debug: RHS of the current level for every instance into V_R.
 template <int C, bool STG>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int b = blockIdx.x / C;
   const uint32_t r = crank<C>();
   const Inst I = inst_view(P, b);
@@ -2063,7 +2214,7 @@ cudaError_t launch_solve_k(K kern, const Plan &pl, const DevParams &dp0, int32_t
         grid = (1 + hcl) * pl.C;
         e = cudaMemsetAsync(dp.sync, 0, 8, st);                 // solver CTA-levels done
         if (e == cudaSuccess) e = cudaMemsetAsync(dp.sync + 1, 0xff, 16, st);   // ready[] = -1
-        if (e == cudaSuccess) e = cudaMemsetAsync(dp.sync + 3, 0, 16, st);      // counters
+        if (e == cudaSuccess) e = cudaMemsetAsync(dp.sync + 3, 0, 24, st);      // counters, gave-up flag
         if (e != cudaSuccess) return e;
       }
     } else {

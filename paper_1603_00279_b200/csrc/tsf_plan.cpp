@@ -56,6 +56,8 @@ static int validate_one(const tsf_problem *p) {
     if (!p->basis || !p->scal) return fail("separable source needs basis and scal arrays");
   } else if (p->src_kind == TSF_SRC_TABLE) {
     if (!p->f_table) return fail("table source needs f_table");
+  } else if (p->src_kind == TSF_SRC_CALLBACK) {
+    if (!p->f_cb) return fail("callback source needs f_cb");
   } else if (p->src_kind != TSF_SRC_ZERO) {
     return fail("unknown src_kind %g", p->src_kind);
   }
@@ -82,8 +84,11 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
     int rc = validate_one(p + b);
     if (rc) return rc;
     if (p[b].n != p[0].n || p[b].M != p[0].M || p[b].src_kind != p[0].src_kind ||
-        (p[0].src_kind == TSF_SRC_SEPARABLE && p[b].K != p[0].K))
-      return fail("instance %g: all instances must share n, M, source kind and K", b);
+        (p[0].src_kind == TSF_SRC_SEPARABLE && p[b].K != p[0].K) ||
+        (p[0].src_kind == TSF_SRC_TABLE && (p[b].f_table_on_device != 0) != (p[0].f_table_on_device != 0)))
+      return fail("instance %g: all instances must share n, M, source kind, K and f table residency", b);
+    if (p[b].f_table_on_device && p[b].src_kind != TSF_SRC_TABLE)
+      return fail("instance %g: f_table_on_device needs the table source", b);
   }
   if (s->method != TSF_BICGSTAB && s->method != TSF_CGNR && s->method != TSF_PCGS && s->method != TSF_GSF) return fail("unknown method %g", s->method);
   if (s->method == TSF_GSF) {
@@ -133,11 +138,15 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.M = p[0].M;
   P.B = B;
   P.K = p[0].src_kind == TSF_SRC_SEPARABLE ? p[0].K : 0;
-  P.src_kind = p[0].src_kind;
+  // a callback source is evaluated at tsf_init into the instance's table (slow path)
+  P.src_kind = p[0].src_kind == TSF_SRC_CALLBACK ? int32_t(TSF_SRC_TABLE) : p[0].src_kind;
   P.method = s->method;
   P.precond = s->precond;
   P.maxit = s->maxit;
   P.tol = s->tol;
+  P.ftab_dev = (p[0].src_kind == TSF_SRC_TABLE && p[0].f_table_on_device) ? 1 : 0;
+  P.x0_warm = s->x0_warm ? 1 : 0;
+  P.true_res = s->true_residual ? 1 : 0;
   const int64_t n = P.n;
   int C = s->cluster;
   if (C == 0) {
@@ -194,6 +203,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.off_sync = o;    o = up(o + 64);
   P.off_pre = o;     o = up(o + (B == 1 ? size_t(2) * size_t(n) * 8 : 0));
   P.off_prof = o;    o = up(o + 32 * 8);
+  P.off_fptr = o;    o = up(o + size_t(B) * 8);
   // init scratch (batched spectra FFTs): per instance 2 x (2n + n) complex
   const size_t per = size_t(3 * n) * 16 * 2;
   int32_t batch = int32_t(std::max<int64_t>(1, std::min<int64_t>(B, (256LL << 20) / int64_t(per))));
@@ -201,21 +211,25 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.off_scratch = o; P.scratch_bytes = per * size_t(batch); o = up(o + P.scratch_bytes);
   P.off_inst = o;
   // per-instance block
+  // host-provided inputs first ([0, o_omega) is one contiguous host image per instance,
+  // uploaded for all instances by a single pitched copy), then device-computed tables
   size_t q = 0;
   P.o_par = q;   q = up(q + 128);
-  P.o_omega = q; q = up(q + size_t(n + 2) * 8);
-  P.o_lwe = q;   q = up(q + size_t(n + 1) * 16);
-  P.o_lwp = q;   q = up(q + size_t(n / 2 + 1) * 16);
   P.o_lev = q;   q = up(q + size_t(P.M) * 32);
   P.o_hwc = q;   q = up(q + size_t(P.M) * 8);
   P.o_hwe = q;   q = up(q + size_t(P.M) * 8);
   P.o_scal = q;  q = up(q + size_t(P.M) * size_t(std::max(P.K, 1)) * 8);
   P.o_basis = q; q = up(q + size_t(std::max(P.K, 1)) * size_t(n) * 8);
-  P.o_ftab = q;  q = up(q + (P.src_kind == TSF_SRC_TABLE ? size_t(P.M) * size_t(n) * 8 : 0));
+  P.o_ftab = q;  q = up(q + (P.src_kind == TSF_SRC_TABLE && !P.ftab_dev ? size_t(P.M) * size_t(n) * 8 : 0));
+  P.o_phi = q;   q = up(q + size_t(n) * 8);
+  P.o_omega = q; q = up(q + size_t(n + 2) * 8);
+  P.o_lwe = q;   q = up(q + size_t(n + 1) * 16);
+  P.o_lwp = q;   q = up(q + size_t(n / 2 + 1) * 16);
   P.o_vec = q;   q = up(q + size_t(kNumVec) * size_t(n) * 8);
   P.o_hist = q;  q = up(q + size_t(P.M) * size_t(n) * 8);
   P.o_it = q;    q = up(q + size_t(P.M) * 4);
   P.o_rr = q;    q = up(q + size_t(P.M) * 8);
+  P.o_trr = q;   q = up(q + size_t(P.M) * 8);
   P.o_st = q;    q = up(q + size_t(P.M) * 4);
   P.o_mul = q;   q = up(q + size_t(n + n / 2) * 16);
   P.o_gsf = q;   q = up(q + (s->method == TSF_GSF ? size_t(4) * size_t(n + 1) * 16 : 0));
@@ -340,7 +354,11 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.o_par = pl.o_par; d.o_omega = pl.o_omega; d.o_lwe = pl.o_lwe; d.o_lwp = pl.o_lwp;
   d.o_lev = pl.o_lev; d.o_hwc = pl.o_hwc; d.o_hwe = pl.o_hwe; d.o_scal = pl.o_scal;
   d.o_basis = pl.o_basis; d.o_ftab = pl.o_ftab; d.o_vec = pl.o_vec; d.o_hist = pl.o_hist;
-  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_st = pl.o_st; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
+  d.o_it = pl.o_it; d.o_rr = pl.o_rr; d.o_trr = pl.o_trr; d.o_st = pl.o_st; d.o_phi = pl.o_phi;
+  d.fptr = reinterpret_cast<const double *const *>(ws + pl.off_fptr);
+  d.ftab_dev = pl.ftab_dev;
+  d.x0_warm = pl.x0_warm;
+  d.true_res = pl.true_res; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
   return d;
 }
 

@@ -16,7 +16,8 @@ namespace tsf {
 constexpr int kThreads = 256;          // threads per CTA
 constexpr int kMaxLocal = 8192;        // max complex elements of the local FFT (128 KiB)
 constexpr int kNumVec = 13;            // u, Krylov work vectors, phi copy, GSF generators x, y
-constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^)
+constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^);
+                                       // g (read once per level) always lives in HBM
 constexpr int64_t kMaxSmem = 232448;   // opt-in dynamic shared memory per CTA (227 KiB)
 constexpr size_t kAlign = 256;
 #ifdef TSF_PAD
@@ -26,7 +27,7 @@ constexpr int kPadBuf = 0;             // XOR-swizzled transform buffers need no
 #endif
 
 // Vector slots inside the per-instance vector block (each n doubles).
-enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_PHI, V_GX, V_GY };
+enum Vec { V_U = 0, V_X, V_R, V_RH, V_P, V_V, V_S, V_T, V_PH, V_SH, V_G, V_GX, V_GY };
 
 // Plain-old-data parameters handed to every kernel by value.
 struct DevParams {
@@ -55,7 +56,11 @@ struct DevParams {
   char *inst;                      // base of instance 0
   int64_t stride;                  // bytes between instances
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf, o_xg;
+  int64_t o_vec, o_hist, o_it, o_rr, o_trr, o_st, o_mul, o_gsf, o_xg, o_phi;
+  const double *const *fptr;       // borrowed device f tables (natural order), one per instance
+  int32_t ftab_dev;                // 1: the source table is read through fptr
+  int32_t x0_warm;                 // NEXT-3: Krylov initial guess u^j (else 0)
+  int32_t true_res;                // compute ||g - A u^{j+1}|| / ||g|| at every level exit
 };
 
 struct Plan {
@@ -73,11 +78,13 @@ struct Plan {
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
   size_t off_level = 0, off_prof = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
-  size_t off_sync = 0, off_pre = 0;
+  size_t off_sync = 0, off_pre = 0, off_fptr = 0;
+  int32_t x0_warm = 0, true_res = 0;
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
-  int64_t o_vec, o_hist, o_it, o_rr, o_st, o_mul, o_gsf, o_xg;
+  int64_t o_vec, o_hist, o_it, o_rr, o_trr, o_st, o_mul, o_gsf, o_xg, o_phi;
+  int32_t ftab_dev = 0;      // source table borrowed from device memory (not copied)
 };
 
 // Per-instance host tables (all doubles).
@@ -144,7 +151,7 @@ TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resid
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;
   if (!staged) c2 += chunk_cplx;                   // chunk buffer of the unstaged column stage
-  int64_t d = 48 + 128 + 4;                        // reductions, push buffers, mbarriers
+  int64_t d = 48 + 128 + 4 + 2;                    // reductions, push buffers, mbarriers, flag
   return 16 * c2 + 8 * d + 64;
 }
 

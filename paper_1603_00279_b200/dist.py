@@ -28,16 +28,29 @@ class BatchResult:
     status: np.ndarray     # [B][M]
 
 
+def collective_device(device=None):
+    """Device of the gather buffers: NCCL needs CUDA tensors (the current device), gloo CPU."""
+    import torch
+    import torch.distributed as dist
+    if device is not None:
+        return torch.device(device)
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def gather(local: BatchResult, B: int, n: int, M: int, device=None) -> BatchResult:
-    """All-gather the per-rank blocks into full [B] arrays on every rank (rank order)."""
+    """All-gather the per-rank blocks into full [B] arrays on every rank (rank order).
+    Blocks may be numpy arrays or torch tensors (a CUDA u^M goes device to device)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size()
+    device = collective_device(device)
     maxb = max(len(shard(B, world, r)) for r in range(world))
     nb = local.u.shape[0]
 
     def pad(a, dtype):
-        t = torch.zeros((maxb,) + a.shape[1:], dtype=dtype, device=device)
+        t = torch.zeros((maxb,) + tuple(a.shape[1:]), dtype=dtype, device=device)
         if nb:
             t[:nb] = torch.as_tensor(a, dtype=dtype, device=device)
         return t

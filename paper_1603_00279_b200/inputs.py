@@ -78,8 +78,9 @@ class Instance:
     gamma: Callable
     dplus: Callable
     dminus: Callable
-    source: str = "mms3"            # "mms3" | "exa" | "table" | "zero"
-    f_table: np.ndarray | None = None
+    source: str = "mms3"            # "mms3" | "exa" | "table" | "callback" | "zero"
+    f_table: np.ndarray | None = None   # [M][n] numpy (copied) or CUDA float64 tensor (borrowed)
+    f_callback: Callable | None = None  # f(x: ndarray, t: float) -> ndarray ("callback")
     phi: Callable = X
     a: float = 0.0
     b: float = 1.0

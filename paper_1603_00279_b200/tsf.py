@@ -59,10 +59,24 @@ def marshal(instances: Sequence[Instance]):
                                                                   inst.dminus, inst.source))
             p.src_kind, p.K = L.SRC_SEPARABLE, 4
             p.basis, p.scal = _pd(arrs["basis"]), _pd(arrs["scal"])
+        elif inst.source == "table" and hasattr(inst.f_table, "data_ptr"):
+            ft = inst.f_table                      # device tensor: borrowed, natural order
+            assert ft.is_cuda and ft.is_contiguous() and tuple(ft.shape) == (inst.M, inst.n)
+            assert str(ft.dtype) == "torch.float64"
+            arrs["f_dev"] = ft                     # keep the tensor alive with the handle
+            p.src_kind, p.f_table, p.f_table_on_device = L.SRC_TABLE, C.cast(C.c_void_p(ft.data_ptr()), L.PD), 1
         elif inst.source == "table":
             arrs["f"] = np.ascontiguousarray(inst.f_table, dtype=np.float64)
             assert arrs["f"].shape == (inst.M, inst.n)
             p.src_kind, p.f_table = L.SRC_TABLE, _pd(arrs["f"])
+        elif inst.source == "callback":
+            fn = inst.f_callback                   # python f(x: ndarray, t: float) -> ndarray
+
+            def _cb(xp, nn, t, outp, _ctx, fn=fn):
+                xa = np.ctypeslib.as_array(xp, shape=(nn,))
+                np.ctypeslib.as_array(outp, shape=(nn,))[:] = fn(xa, t)
+            arrs["cb"] = L.SRC_CB(_cb)
+            p.src_kind, p.f_cb = L.SRC_CALLBACK, arrs["cb"]
         elif inst.source == "zero":
             p.src_kind = L.SRC_ZERO
         else:
@@ -71,13 +85,16 @@ def marshal(instances: Sequence[Instance]):
     return probs, keep
 
 
-def make_solver_struct(method="bicgstab", precond="strang", tol=1e-12, maxit=None, cluster=0):
+def make_solver_struct(method="bicgstab", precond="strang", tol=1e-12, maxit=None, cluster=0,
+                       x0_warm=False, true_residual=True):
     s = L.TsfSolver()
     s.method = METHODS[method]
     s.precond = PRECONDS[precond]
     s.tol = tol
     s.maxit = maxit if maxit is not None else (5000 if method == "cgnr" else 1000)
     s.cluster = cluster
+    s.x0_warm = int(bool(x0_warm))
+    s.true_residual = int(bool(true_residual))
     return s
 
 
@@ -94,15 +111,17 @@ class Solver:
     """A batch of instances (same n, M) solved level by level on one GPU."""
 
     def __init__(self, instances: Sequence[Instance], method="bicgstab", precond="strang",
-                 tol=1e-12, maxit=None, cluster=0, device=None, stream=None, workspace=None):
+                 tol=1e-12, maxit=None, cluster=0, device=None, stream=None, workspace=None,
+                 x0_warm=False, true_residual=True):
         import torch
         self.lib = L.load()
         self.instances = list(instances)
         self.B = len(self.instances)
         self.n, self.M = self.instances[0].n, self.instances[0].M
         probs, keep = marshal(self.instances)
-        self.h2d_bytes = sum(a.nbytes for arrs in keep for a in arrs.values())
-        self._solver = make_solver_struct(method, precond, tol, maxit, cluster)
+        self.h2d_bytes = sum(a.nbytes for arrs in keep for a in arrs.values() if isinstance(a, np.ndarray))
+        self._borrowed = [arrs["f_dev"] for arrs in keep if "f_dev" in arrs]
+        self._solver = make_solver_struct(method, precond, tol, maxit, cluster, x0_warm, true_residual)
         info = L.TsfPlanInfo()
         L.check(self.lib.tsf_plan(probs, self.B, C.byref(self._solver), C.byref(info)), "tsf_plan")
         self.info = info
@@ -113,6 +132,10 @@ class Solver:
         else:
             self.workspace = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        if self.stream != torch.cuda.current_stream(dev):
+            # allocated on the current stream, used on self.stream: keep the caching allocator
+            # from reusing it while the handle's kernels may still run
+            self.workspace.record_stream(self.stream)
         h = C.c_void_p()
         L.check(self.lib.tsf_init(probs, self.B, C.byref(self._solver),
                                   C.c_void_p(self.workspace.data_ptr()), C.c_size_t(int(info.workspace_bytes)),
@@ -160,6 +183,12 @@ class Solver:
                                        st.ctypes.data_as(C.POINTER(C.c_int32))), "tsf_get_stats")
         return it, rr, st
 
+    def true_residuals(self) -> np.ndarray:
+        """||g - A u^{j+1}|| / ||g|| per level ([B][M]; 0 where not computed)."""
+        out = np.zeros((self.B, self.M))
+        L.check(self.lib.tsf_get_true_residuals(self.h, _pd(out)), "tsf_get_true_residuals")
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.tsf_destroy(self.h)
@@ -183,6 +212,12 @@ class Solver:
         ms = C.c_float(0.0)
         L.check(self.lib.tsf_debug_apply_bench(self.h, inst, j, reps, C.byref(ms)), "tsf_debug_apply_bench")
         return ms.value
+
+    def debug_helper_state(self) -> np.ndarray:
+        out = np.zeros(8, dtype=np.int64)
+        L.check(self.lib.tsf_debug_helper_state(self.h, out.ctypes.data_as(C.POINTER(C.c_int64))),
+                "tsf_debug_helper_state")
+        return out
 
     def debug_spectra(self, inst: int, j: int):
         la = np.zeros(2 * (self.n + 1))

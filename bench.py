@@ -109,6 +109,19 @@ def algorithmic_bytes(n, M, iters_half_rows, method, src_units):
     return total
 
 
+def CONFIGS_ALL_get():
+    from paper_1603_00279_b200.inputs import CONFIGS
+    return CONFIGS
+
+
+class _Cfgs:
+    def __getitem__(self, k):
+        return CONFIGS_ALL_get()[k]
+
+
+CONFIGS_ALL = _Cfgs()
+
+
 def build_instances(cfg, world, rank):
     from paper_1603_00279_b200 import dist
     from paper_1603_00279_b200.inputs import CONFIGS
@@ -143,9 +156,31 @@ def oracle_problem(inst):
                 dminus=enc(inst.dminus), src=src)
 
 
+def host_cpu():
+    """Host CPU model and the oracle's thread count (cpu_baseline is run on all host cores)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return model, threads
+
+
 def oracle_rate(cfg):
-    """Oracle levels/s for `cfg`, from a bounded sample (10-30 s of CPU work) extrapolated
-    to the full size: dense GE is O(n^3) per factorization and O(n^2) per level."""
+    """Oracle levels/s for `cfg` on all host cores (OpenMP over independent rows; the oracle's
+    arithmetic is unchanged), from a bounded sample of its OWN steps at the FULL size n
+    (orc_time_sample): the dense assembly, the first kmax columns of the elimination and one
+    level's RHS + LU solve + 3 refinement steps at the longest history.  The full run is
+      constant coefficients (LU reuse):  2 (assembly + factorization) + M level
+      variable coefficients (a factorization per level):  M (assembly + factorization + level)
+    with the factorization's untimed columns k >= kmax scaled by the (n-k)^2 work of the plain
+    row-update loop.  C5 (n = 2^17: the dense matrices need 3 x 128 GiB) is timed at n = 4096 and
+    scaled by n^3 (factorization) / n^2 (level): labelled as an extrapolation."""
     import numpy as np
 
     import oracle as O
@@ -155,36 +190,49 @@ def oracle_rate(cfg):
     kw = oracle_problem(inst)
     n, M, B = inst.n, inst.M, len(insts)
     const = all(kw[k][0] == O.CONST for k in ("gamma", "dplus", "dminus"))
-    ns = min(n, 1024 if const else 512)
-    ns = ns - 1 if ns == n else ns      # any n is fine for the oracle
+    ns = n if n <= 16384 else 4096
+    p = O.Problem(n=ns, M=M, **kw)
+    if p.src == O.SRC_TABLE:
+        p.f_table = np.ascontiguousarray(inst.f_table[:M, :ns])
+    j = M - 1
+    U = np.ascontiguousarray(np.random.default_rng(0).standard_normal((j + 1, ns)) * 1e-3)
+    kmax = ns if ns <= 2048 else 64
+    t0 = time.perf_counter()
+    ta, tf, tl = O.time_sample(p, j, kmax, U)
+    wall = time.perf_counter() - t0
+    k = np.arange(ns, dtype=np.float64)
+    work = (ns - k) ** 2
+    fact = tf * work.sum() / work[:kmax].sum()
+    if const:
+        full = 2 * (ta + fact) + M * tl
+    else:
+        full = M * (ta + fact + tl)
+    label = "measured at full n" if ns == n else f"measured at n={ns}, scaled to n={n} by n^3 / n^2"
+    if ns != n:
+        s3, s2 = (n / ns) ** 3, (n / ns) ** 2
+        full = (2 * (ta * s2 + fact * s3) + M * tl * s2) if const else M * (ta * s2 + fact * s3 + tl * s2)
+    model, threads = host_cpu()
+    sample = (f"oracle (dense GE, {'LU reuse' if const else 'factorization per level'}, 3 refinement steps) "
+              f"on {cfg}, {label}: assembly {ta:.2f}s, elimination columns 0..{kmax - 1} of {ns} {tf:.2f}s "
+              f"(all {ns} columns: {fact:.1f}s by the (n-k)^2 work law), one level at history {j} {tl:.2f}s; "
+              f"full run = {full:.0f}s per instance ({wall:.0f}s sampled); {threads} OpenMP threads on "
+              f"'{model}'; gcc -O2 -ffp-contract=off -fopenmp")
+    return M / full, sample, full * B, threads
 
-    def run(nn, MM):
-        p = O.Problem(n=nn, M=MM, **kw)
-        if p.src == O.SRC_TABLE:
-            p.f_table = np.ascontiguousarray(inst.f_table[:MM, :nn])
-        t0 = time.perf_counter()
-        O.solve(p)
-        return time.perf_counter() - t0
-    if const:     # LU reuse: 2 factorizations + per-level triangular solves
-        Ms = min(M, 64)
-        t2 = run(ns, 2)
-        tm = run(ns, Ms)
-        per_level = max((tm - t2) / (Ms - 2), 1e-9)
-        fact = max(t2 - 2 * per_level, 1e-9)
-        s = n / ns
-        full = fact * s**3 + M * per_level * s**2
-        sample = (f"oracle (dense GE, LU reuse) on {cfg} params at n={ns}: 2 levels {t2:.2f}s, "
-                  f"{Ms} levels {tm:.2f}s; extrapolated to n={n}, M={M} as fact*(n/ns)^3 + "
-                  f"M*level*(n/ns)^2 = {full:.1f}s per instance")
-    else:         # variable coefficients: one factorization per level
-        Ms = 4
-        tm = run(ns, Ms)
-        per_level = tm / Ms
-        s = n / ns
-        full = M * per_level * s**3
-        sample = (f"oracle (dense GE per level) on {cfg} params at n={ns}, {Ms} levels {tm:.2f}s; "
-                  f"extrapolated to n={n}, M={M} as M*level*(n/ns)^3 = {full:.1f}s per instance")
-    return M / full, sample, full * B
+
+def lib_hash() -> str:
+    import hashlib
+    from paper_1603_00279_b200 import _lib as L
+    h = hashlib.sha256()
+    with open(L.LIB_PATH, "rb") as fh:
+        for chunk in iter(lambda: fh.read(1 << 24), b""):
+            h.update(chunk)
+    return h.hexdigest()[:16]
+
+
+def traffic_key(args) -> str:
+    return f"{args.config}/{args.method}/{args.precond}" + ("/warm" if args.warm else "") + \
+        ("/tres" if args.true_res else "")
 
 
 def base_config(args):
@@ -201,11 +249,12 @@ def run_reference(args):
         return
     vals = []
     sample = ""
+    threads = 1
     for _ in range(args.warmup):
         oracle_rate(args.config)
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        v, sample, _ = oracle_rate(args.config)
+        v, sample, _, threads = oracle_rate(args.config)
         vals.append((v, time.perf_counter() - t0))
     value = statistics.median(v for v, _ in vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "levels/s",
@@ -213,7 +262,7 @@ def run_reference(args):
             "ms_per_step": 1000 * statistics.mean(t for _, t in vals), "higher_is_better": True,
             "scaling": "weak" if args.config in ("C1", "C2", "C3") else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": base_config(args),
-            "cpu_baseline": {"value": value, "unit": "levels/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "levels/s", "cores": threads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "levels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -232,7 +281,9 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-true-res", action="store_true", help="skip the per-level true residual")
+    ap.add_argument("--true-res", action="store_true",
+                    help="also compute the per-level true residual (an extra A application per level; "
+                         "off by default: the paper's stopping rule uses the recurrence residual, P:922-924)")
     ap.add_argument("--warm", action="store_true", help="NEXT-3 warm start x0 = u^j")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -275,7 +326,7 @@ def main():
     insts, scaling, units_total = build_instances(args.config, world, rank)
     n, M = insts[0].n, insts[0].M
     solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster,
-                     true_residual=not args.no_true_res, x0_warm=args.warm)
+                     true_residual=args.true_res, x0_warm=args.warm)
     stream = torch.cuda.Stream(dev)
     t_init0 = time.perf_counter()
     s = tsf.Solver(insts, stream=stream, **solver_kw)
@@ -287,9 +338,24 @@ def main():
         s.solve()
         rc = s.sync()
         assert rc >= 0, rc
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters_total = 0.0
-    ms = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # batched configs under torchrun: the step ends after the NCCL all-gather of u^M and the
+    # per-level statistics ("from the barrier before the first level to the end of
+    # the gather"); u^M goes device to device (tsf_get_solutions into a CUDA tensor)
+    do_gather = world > 1 and scaling == "strong"
+    ubuf = torch.empty((len(insts), n), dtype=torch.float64, device=dev) if do_gather else None
+    B_total = len(CONFIGS_ALL[args.config]()) if do_gather else 0
+
+    def gather_results():
+        from paper_1603_00279_b200 import dist as D
+        s.solution_into(ubuf)
+        it, rr, st = s.stats()
+        with torch.cuda.stream(stream):
+            res = D.gather(D.BatchResult(ubuf, it, rr, st), B_total, n, M, device=dev)
+        return res
+
+    ms, kms, gms = [], [], []
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             s.reset()
@@ -301,11 +367,18 @@ def main():
             ev[k][0].record(stream)
             s.solve()
             ev[k][1].record(stream)
+            if do_gather:
+                res = gather_results()
+            ev[k][2].record(stream)
             torch.cuda.synchronize()
             barrier()
-            ms.append(ev[k][0].elapsed_time(ev[k][1]))
+            ms.append(ev[k][0].elapsed_time(ev[k][2]))
+            kms.append(ev[k][0].elapsed_time(ev[k][1]))
+            gms.append(ev[k][1].elapsed_time(ev[k][2]))
             rc = s.sync()
             assert rc >= 0, rc
+            if do_gather:
+                assert res.u.shape == (B_total, n) and (res.status == 0).all()
     it_half, relres, status = s.stats()
     iters_local = float(it_half.sum()) / 2.0
     t_step_ms = allmax(statistics.mean(ms))
@@ -316,14 +389,23 @@ def main():
     iters_per_s = iters_job * args.steps / total_s
     src_units = 1 if insts[0].source == "table" else (4 if insts[0].source in ("mms3", "exa") else 0)
     abytes = algorithmic_bytes(n, M, it_half, args.method, src_units)   # per launch, this rank
-    achieved = abytes / (statistics.mean(ms) / 1000.0) / 1e9
+    kernel_s = statistics.mean(kms) / 1000.0       # the k_solve launch, CUDA events on its stream
+    achieved = abytes / kernel_s / 1e9
     peak, peak_kind = peaks()
-    traffic = None
+    # ncu DRAM bytes of the same launch (profiles/traffic.json, written by tools/ncu_traffic.py),
+    # accepted only if captured with this exact libtsf.so
+    traffic, traffic_note = None, "no capture"
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(f"{args.config}/{args.method}/{args.precond}")
-    except Exception:
-        pass
+            ent = json.load(fh).get(traffic_key(args))
+        if ent is None:
+            traffic_note = "no capture for this workload"
+        elif ent.get("lib") != lib_hash():
+            traffic_note = f"stale capture (lib {ent.get('lib')} != {lib_hash()})"
+        else:
+            traffic, traffic_note = float(ent["dram_bytes"]), f"ncu {ent.get('when', '')}"
+    except Exception as e:  # noqa: BLE001
+        traffic_note = f"unreadable: {e}"
 
     # ---- end to end through the public API: host inputs -> device, solve, results -> host
     e2e = None
@@ -348,8 +430,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample, _ = oracle_rate(args.config)
-        cpu = {"value": v, "unit": "levels/s", "cores": 1, "kind": "oracle", "sample": sample}
+        v, sample, _, threads = oracle_rate(args.config)
+        cpu = {"value": v, "unit": "levels/s", "cores": threads, "kind": "oracle", "sample": sample}
 
     if rank == 0:
         info = s.info
@@ -359,17 +441,25 @@ def main():
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {**base_config(args), "instances": units_total, "cluster": info.cluster,
-                       "l2": "flushed between steps (512 MiB write)"},
+                       "exchange": ["local", "staged DSMEM push", "chunked via L2"][info.exchange],
+                       "true_residual": bool(args.true_res), "x0_warm": bool(args.warm),
+                       "l2": "flushed between steps (512 MiB write)",
+                       "timed": "k_solve + level counter" + (" + NCCL all-gather of u^M and stats" if do_gather else "")},
             "krylov_iters_per_s": iters_per_s,
             "mean_iters_per_level": iters_job / levels_job,
             "init_s": t_init,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "k_solve (one launch = all M levels of the rank's batch)",
-                         "algorithmic_bytes_per_launch": abytes},
+                         "kernel_ms": 1000.0 * kernel_s,
+                         "algorithmic_bytes_per_launch": abytes,
+                         "ncu_dram_gbs": (traffic / kernel_s / 1e9) if traffic else None,
+                         "ncu_dram_frac": (traffic / kernel_s / 1e9 / peak) if traffic else None,
+                         "traffic_source": traffic_note},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (3 if do_gather else 2) * args.steps,
+            "gather_ms_per_step": allmax(statistics.mean(gms)) if do_gather else None,
             "clocks": clk.summary(),
             "max_relres": float(relres.max()),
             "status_ok": bool((status == 0).all()),

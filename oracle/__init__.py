@@ -73,6 +73,7 @@ def lib():
             "orc_rhs_nodense": (C.c_int, [pp, i64, pd, pd]),
             "orc_solve": (C.c_int, [pp, pd]),
             "orc_solve_level": (C.c_int, [pp, i64, pd, pd]),
+            "orc_time_sample": (C.c_int, [pp, i64, i64, pd, pd]),
             "orc_l2": (d, [i64, d, pd]),
             "orc_dft": (None, [i64, pd, pd, C.c_int]),
             "orc_fft_plan": (C.c_int, [i64, pi32]),
@@ -246,6 +247,17 @@ def solve_level(p: Problem, j: int, U: np.ndarray) -> np.ndarray:
     cp = p.c()
     assert lib().orc_solve_level(C.byref(cp), j, _pd(U), _pd(out)) == 0
     return out
+
+
+def time_sample(p: Problem, j: int, kmax: int, U: np.ndarray) -> np.ndarray:
+    """Wall seconds [assembly, first kmax elimination columns, one level at history j] of the
+    oracle's own steps at the full size (bench.py cpu_baseline; no result is returned)."""
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    assert U.shape == (j + 1, p.n)
+    t = np.zeros(3)
+    cp = p.c()
+    assert lib().orc_time_sample(C.byref(cp), j, kmax, _pd(U), _pd(t)) >= 0
+    return t
 
 
 def l2(v: np.ndarray, h: float) -> float:

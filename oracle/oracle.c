@@ -209,8 +209,8 @@ int orc_exact(const orc_problem *p, double t, double *u) {
 /* ---------------------------------------------------------------------------------- */
 /* Gaussian elimination with partial pivoting, row-major, factors kept for reuse
  * ("[L,U]=lu(A); x = U\(L\b)").                                           */
-static int lu_factor(int64_t n, double *A, int64_t *piv) {
-  for (int64_t k = 0; k < n; ++k) {
+static int lu_factor_k(int64_t n, double *A, int64_t *piv, int64_t kmax) {
+  for (int64_t k = 0; k < kmax; ++k) {
     int64_t pr = k;
     double best = fabs(A[k * n + k]);
     for (int64_t i = k + 1; i < n; ++i)
@@ -235,6 +235,8 @@ static int lu_factor(int64_t n, double *A, int64_t *piv) {
   }
   return 0;
 }
+
+static int lu_factor(int64_t n, double *A, int64_t *piv) { return lu_factor_k(n, A, piv, n); }
 
 static void lu_solve(int64_t n, const double *LU, const int64_t *piv, double *x) {
   for (int64_t k = 0; k < n; ++k) {
@@ -534,4 +536,44 @@ void orc_tchan_col(int64_t n, const double *col, const double *row, double *c) {
   c[0] = col[0];
   for (int64_t k = 1; k < n; ++k)
     c[k] = ((double)(n - k) * col[k] + (double)k * row[n - k]) / (double)n;
+}
+
+/* ---------------------------------------------------------------------------------- */
+/* Timing sample of orc_solve's own steps at the full size n (bench.py cpu_baseline): wall
+ * seconds of (t[0]) the dense assembly of A and B, (t[1]) the first kmax column steps of
+ * lu_factor, (t[2]) one level's remaining work at history length j: the RHS (dense B u^j,
+ * memory term over j rows, source), lu_solve and 3 refinement steps.  The level work is timed on
+ * the partially eliminated matrix: its cost does not depend on the values.  U[(j+1)][n].  */
+#include <time.h>
+static double wall_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+int orc_time_sample(const orc_problem *p, int64_t j, int64_t kmax, const double *U, double *t) {
+  if (!grid_ok(p) || j < 0 || j >= p->M || kmax < 1 || kmax > p->n) return -1;
+  const int64_t n = p->n;
+  double *A = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *A0 = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *B = (double *)malloc(sizeof(double) * (size_t)(n * n));
+  double *g = (double *)malloc(sizeof(double) * (size_t)n);
+  double *rhs = (double *)malloc(sizeof(double) * (size_t)n);
+  int64_t *piv = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+  if (!A || !A0 || !B || !g || !rhs || !piv) return -2;
+  double t0 = wall_s();
+  orc_assemble(p, j, A, B);
+  memcpy(A0, A, sizeof(double) * (size_t)(n * n));
+  t[0] = wall_s() - t0;
+  t0 = wall_s();
+  int rc = lu_factor_k(n, A, piv, kmax);
+  t[1] = wall_s() - t0;
+  for (int64_t k = kmax; k < n; ++k) piv[k] = k;
+  t0 = wall_s();
+  rhs_with_B(p, j, U, B, g);
+  memcpy(rhs, g, sizeof(double) * (size_t)n);
+  lu_solve(n, A, piv, g);
+  refine(n, A0, A, piv, rhs, g, 3);
+  t[2] = wall_s() - t0;
+  free(A); free(A0); free(B); free(g); free(rhs); free(piv);
+  return rc;
 }

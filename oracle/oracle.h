@@ -70,6 +70,10 @@ int orc_solve(const orc_problem *p, double *U);
 /* Same, but solve level j only from a given history (teacher forcing): out[n]. */
 int orc_solve_level(const orc_problem *p, int64_t j, const double *U, double *out);
 
+/* Timing sample at full n for bench.py (see oracle.c): t[3] = assembly, first kmax columns of
+ * the elimination, one level's RHS + solve + refinement at history length j.  U[(j+1)][n]. */
+int orc_time_sample(const orc_problem *p, int64_t j, int64_t kmax, const double *U, double *t);
+
 /* Discrete L2 norm: sqrt(h sum v_i^2). */
 double orc_l2(int64_t n, double h, const double *v);
 

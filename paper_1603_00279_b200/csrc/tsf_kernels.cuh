@@ -167,6 +167,14 @@ __device__ __forceinline__ int64_t ld_acquire(const int64_t *p) {
 __device__ __forceinline__ void st_release(int64_t *p, int64_t v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// 16-byte asynchronous global -> shared copy through L2 (LDGSTS): no register staging, so a
+// thread can keep many loads in flight without raising register pressure
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t gtimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -249,7 +257,7 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   double2 *c = reinterpret_cast<double2 *>(raw);
   s.A = c; c += L1e + kPadBuf * (L1e / 16);
   if (staged) { s.B = c; c += L1e; s.O = c; c += L1e + kPadBuf * (L1e / 16); }
-  else if (chunk > 0) { s.B = c; c += 2 * chunk * C; }
+  else if (chunk > 0) { s.B = c; c += 5 * chunk * C; }   // chunk buffer [2 chunk C] + 3 prefetched tables
   if (resident) {
     s.twd = c; c += L1e;
     s.ctwe = c; c += L1e; s.ctwp = c; c += L1p;
@@ -1001,20 +1009,37 @@ __device__ __forceinline__ void col_twiddles(double2 w, double2 (&wq)[C]) {
 template <int C>
 __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, const Geo &g, const SpecOp &op,
                                               const double2 *__restrict__ tw, uint32_t r, const Smem &sm,
-                                              const double2 *__restrict__ xg) {
+                                              double2 *__restrict__ xg) {
   TSF_PT0();
   const int L1 = g.L1, np = g.np, l1 = g.l1;
   const int W = 2 * CP;                       // columns per chunk
+  // Every global (L2) access below is latency bound (~600-900 cycles per dependent round trip):
+  // each thread issues a batch of independent loads before using any of them (memory-level
+  // parallelism; one load in flight per thread gave ~7 B/clk/SM for the 128 KiB pull).
+  const bool pre = op.mul != nullptr && !op.mul_sh && op.pw == nullptr;
+  double2 *Ta = Bc + 2 * CP * C, *Tb = Ta + CP * C, *Tw = Tb + CP * C;
   for (int c0 = 0; c0 < np; c0 += CP) {
     const int cp = np - c0 < CP ? np - c0 : CP;
     // pull: item u -> (row q, chunk column col); the rows come from the peers' local FFT outputs
-    // staged in L2 (xg[q][slot], written by the caller before its cluster barrier): ~10x the
-    // per-SM bandwidth of DSMEM loads (measured 6-10 B/clk/SM)
-    for (int u = threadIdx.x; u < C * 2 * cp; u += kThreads) {
+    // staged in L2 (xg[q][slot], written by the caller before its cluster barrier); async
+    // copies, all of a thread's in flight at once
+    const int tot = C * 2 * cp;
+    for (int u = threadIdx.x; u < tot; u += kThreads) {
       const int q = u / (2 * cp), col = u - q * (2 * cp);
       const int k1 = col_k1(L1, C, r, 2 * c0 + col);
-      Bc[q * W + col] = __ldcg(xg + q * L1 + dslot(k1, l1));
+      cp_async16(Bc + q * W + col, xg + q * L1 + dslot(k1, l1));
     }
+    // the bin-pair stage's multipliers (task-order table, contiguous in i) and split twiddles,
+    // prefetched with the pull so their L2 latency overlaps it
+    if (pre) {
+      for (int u = threadIdx.x; u < C * cp; u += kThreads) {
+        const int k2 = u / cp, i = c0 + (u - k2 * cp);
+        cp_async16(Ta + u, op.mul + ((op.rC + k2) * 2 + 0) * np + i);
+        cp_async16(Tb + u, op.mul + ((op.rC + C - 1 - k2) * 2 + 1) * np + i);
+        cp_async16(Tw + u, tw + int64_t(int(r) + i * C + L1 * k2) * g.tw2L);
+      }
+    }
+    cp_async_wait_all();
     __syncthreads();
     TSF_PACC(sm, PS_GATHER);
     for (int col = threadIdx.x; col < 2 * cp; col += kThreads) {   // column DFT_C
@@ -1032,55 +1057,82 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
     }
     __syncthreads();
     TSF_PACC(sm, PS_COLF);
-    // bin pairs: item u = k2 * cp + il; (row k2, col (il,0)) <-> (row C-1-k2, col (il,1))
-    for (int u = threadIdx.x; u < C * cp; u += kThreads) {
-      const int k2 = u / cp, il = u - k2 * cp, i = c0 + il;
-      const int pi = int(r) + i * C;
-      if (pi != 0) {
-        const int bin = pi + L1 * k2;
-        double2 &za = Bc[k2 * W + 2 * il];
-        double2 &zb = Bc[(C - 1 - k2) * W + 2 * il + 1];
-        double2 a = za, b = zb;
-        pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
-                   op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
-        za = a;
-        zb = b;
-      } else {
-        const int kk = (C - k2) % C;
-        if (k2 <= C / 2) {                      // column 0: bins L1 k2 <-> L1 (C - k2)
-          const int bin = L1 * k2;
-          const double2 la = op.get(k2, 0, 0, bin);
-          const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
-          double2 &za = Bc[k2 * W];
-          if (kk == k2) {
-            double2 a = za;
-            pair_self(a, la, k2 == 0 ? op.nyqe : la, w, op.scale);
-            za = a;
-          } else {
-            double2 &zb = Bc[kk * W];
-            double2 a = za, b = zb;
-            pair_apply(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
-            za = a;
-            zb = b;
+    // bin pairs: item u = k2 * cp + il; (row k2, col (il,0)) <-> (row C-1-k2, col (il,1)); the
+    // multiplier / twiddle table loads of PU items are issued together.  The pseudo column pair
+    // pi = 0 (CTA 0, first chunk) is done afterwards, one row per thread.
+    constexpr int PU = 1;            // more items per batch spilled the 255-register kernel
+    const int nit = C * cp;
+    for (int u0 = threadIdx.x; u0 < nit; u0 += PU * kThreads) {
+      double2 la[PU], lb[PU], w[PU];
+      int ia[PU], ib[PU];
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        const int u = u0 + k * kThreads;
+        ia[k] = -1;
+        if (u < nit) {
+          const int k2 = u / cp, il = u - k2 * cp, i = c0 + il;
+          const int pi = int(r) + i * C;
+          if (pi != 0) {
+            const int bin = pi + L1 * k2;
+            if (pre) {
+              la[k] = op.conj ? cconj(Ta[u]) : Ta[u];
+              lb[k] = op.conj ? cconj(Tb[u]) : Tb[u];
+              w[k] = Tw[u];
+            } else {
+              la[k] = op.get(k2, 0, i, bin);
+              lb[k] = op.get(C - 1 - k2, 1, i, g.L - bin);
+              w[k] = op.wtw(k2, 0, i, bin, tw, g.tw2L);
+            }
+            ia[k] = k2 * W + 2 * il;
+            ib[k] = (C - 1 - k2) * W + 2 * il + 1;
           }
         }
-        const int km = C - 1 - k2;
-        if (k2 < (C + 1) / 2) {                 // column L1/2: bins L1/2 + L1 k2 <-> k2' = C-1-k2
-          const int bin = L1 / 2 + L1 * k2;
-          const double2 la = op.get(k2, 1, 0, bin);
-          const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
-          double2 &za = Bc[k2 * W + 1];
-          if (km == k2) {
-            double2 a = za;
-            pair_self(a, la, la, w, op.scale);
-            za = a;
-          } else {
-            double2 &zb = Bc[km * W + 1];
-            double2 a = za, b = zb;
-            pair_apply(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
-            za = a;
-            zb = b;
-          }
+      }
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        if (ia[k] < 0) continue;
+        double2 a = Bc[ia[k]], b = Bc[ib[k]];
+        pair_apply(a, b, la[k], lb[k], w[k], op.scale);
+        Bc[ia[k]] = a;
+        Bc[ib[k]] = b;
+      }
+    }
+    if (r == 0 && c0 == 0 && threadIdx.x < C) {
+      const int k2 = threadIdx.x;
+      const int kk = (C - k2) % C;
+      if (k2 <= C / 2) {                      // column 0: bins L1 k2 <-> L1 (C - k2)
+        const int bin = L1 * k2;
+        const double2 la = op.get(k2, 0, 0, bin);
+        const double2 w = op.wtw(k2, 0, 0, bin, tw, g.tw2L);
+        double2 &za = Bc[k2 * W];
+        if (kk == k2) {
+          double2 a = za;
+          pair_self(a, la, k2 == 0 ? op.nyqe : la, w, op.scale);
+          za = a;
+        } else {
+          double2 &zb = Bc[kk * W];
+          double2 a = za, b = zb;
+          pair_apply(a, b, la, op.get(kk, 0, 0, g.L - bin), w, op.scale);
+          za = a;
+          zb = b;
+        }
+      }
+      const int km = C - 1 - k2;
+      if (k2 < (C + 1) / 2) {                 // column L1/2: bins L1/2 + L1 k2 <-> k2' = C-1-k2
+        const int bin = L1 / 2 + L1 * k2;
+        const double2 la = op.get(k2, 1, 0, bin);
+        const double2 w = op.wtw(k2, 1, 0, bin, tw, g.tw2L);
+        double2 &za = Bc[k2 * W + 1];
+        if (km == k2) {
+          double2 a = za;
+          pair_self(a, la, la, w, op.scale);
+          za = a;
+        } else {
+          double2 &zb = Bc[km * W + 1];
+          double2 a = za, b = zb;
+          pair_apply(a, b, la, op.get(km, 1, 0, g.L - bin), w, op.scale);
+          za = a;
+          zb = b;
         }
       }
     }
@@ -1096,9 +1148,11 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
       col_twiddles<C>(tw[k1 * g.twL], wq);
 #pragma unroll
       for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], wq[q]);
-      const int s = pidx(dslot(k1, l1));
+      // back into the L2 staging rows, in place: the slots of a column pair are read and written
+      // only by the pair's owner (L2 stores run at ~10x the per-SM rate of DSMEM stores)
+      const int sl = dslot(k1, l1);
 #pragma unroll
-      for (int q = 0; q < C; ++q) remote<C>(A, uint32_t(q))[s] = z[q];
+      for (int q = 0; q < C; ++q) __stcg(xg + q * L1 + sl, z[q]);
     }
     __syncthreads();                            // Bc is refilled by the next chunk
     TSF_PACC(sm, PS_COLI);
@@ -1132,12 +1186,20 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
       cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs);
       Y = sm.O;
     } else {
-      for (int p = threadIdx.x; p < g.L1; p += kThreads) xg[int64_t(r) * g.L1 + p] = sm.A[pidx(p)];
+      for (int p = threadIdx.x; p < g.L1; p += kThreads) __stcg(xg + int64_t(r) * g.L1 + p, sm.A[pidx(p)]);
       csync<C>();                // every local transform staged in L2 before the gathers
       TSF_PACC(sm, PS_BAR1);
       cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r, sm, xg);
-      csync<C>();                // every push landed before the local inverse transforms
+      TSF_PTR();
+      csync<C>();                // every column result back in L2 before the row reads
       TSF_PACC(sm, PS_BAR3);
+      {                          // this CTA's row back from L2 (async copies, all in flight)
+        const double2 *xr = xg + int64_t(r) * g.L1;
+        for (int p = threadIdx.x; p < g.L1; p += kThreads) cp_async16(sm.A + pidx(p), xr + p);
+        cp_async_wait_all();
+      }
+      __syncthreads();
+      TSF_PACC(sm, PS_SCATTER);
     }
     TSF_PTR();
   }

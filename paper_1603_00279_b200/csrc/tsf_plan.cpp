@@ -183,12 +183,12 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
     if (const char *ev = std::getenv("TSF_VSMEM")) P.vsmem = (with <= kMaxSmem) ? std::atoi(ev) : 0;
   }
   P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem);
-  if (C > 1 && !P.staged) {      // chunk buffer: the largest power-of-two pair count that fits
-    int chunk = P.npe;
-    while (chunk > 1 && P.smem + int64_t(2) * chunk * C * 16 > kMaxSmem) chunk /= 2;
+  if (C > 1 && !P.staged) {      // chunk buffer [2 chunk C] + 3 prefetched pair tables [chunk C]:
+    int chunk = P.npe;             // the largest power-of-two pair count that fits
+    while (chunk > 1 && P.smem + int64_t(5) * chunk * C * 16 > kMaxSmem) chunk /= 2;
     if (const char *ec = std::getenv("TSF_CHUNK")) chunk = std::min(chunk, std::max(1, std::atoi(ec)));
     P.chunk = chunk;
-    P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem, int64_t(2) * chunk * C);
+    P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem, int64_t(5) * chunk * C);
   }
   if (const char *ef = std::getenv("TSF_FUSE_MIN")) P.fuse_min = std::atoi(ef);
 

@@ -400,6 +400,8 @@ def main():
             ent = json.load(fh).get(traffic_key(args))
         if ent is None:
             traffic_note = "no capture for this workload"
+        elif not isinstance(ent, dict):
+            traffic_note = "stale capture (no library hash recorded)"
         elif ent.get("lib") != lib_hash():
             traffic_note = f"stale capture (lib {ent.get('lib')} != {lib_hash()})"
         else:

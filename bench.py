@@ -443,7 +443,7 @@ def main():
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {**base_config(args), "instances": units_total, "cluster": info.cluster,
-                       "exchange": ["local", "staged DSMEM push", "chunked via L2"][info.exchange],
+                       "exchange": ["local", "staged DSMEM push", "chunked via L2", "multi-pass via L2"][info.exchange],
                        "true_residual": bool(args.true_res), "x0_warm": bool(args.warm),
                        "l2": "flushed between steps (512 MiB write)",
                        "timed": "k_solve + level counter" + (" + NCCL all-gather of u^M and stats" if do_gather else "")},

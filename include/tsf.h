@@ -21,7 +21,9 @@
  *    CUDA device memory of the handle's device.
  *  - Every function returns TSF_OK (0) or a negative TSF_E_* code; tsf_last_error()
  *    returns a thread-local message describing the last failure.
- *  - n must be a power of two in [64, 131072]; M >= 1.  B (instances per handle) >= 1.
+ *  - n must be a power of two in [64, 1048576]; M >= 1.  B (instances per handle) >= 1.
+ *    n <= 2^17 keeps every local FFT in shared memory; n = 2^18..2^20 (FFT lengths up to 2^21
+ *    real) runs the multi-pass regime on 16-CTA clusters (plan exchange 3).
  *  - The caller owns the device workspace (e.g. a torch uint8 tensor) and every output
  *    buffer.  All input arrays are copied during tsf_init; nothing is borrowed.
  *  - A handle is bound to one device and one CUDA stream and is not thread-safe.
@@ -132,7 +134,9 @@ typedef struct {
   int64_t precond_len;        /* complex FFT length of the n-point preconditioner (n/2)*/
   size_t workspace_bytes;     /* device workspace required                             */
   int32_t exchange;           /* cross-CTA column stage: 0 none (cluster 1), 1 staged
-                                 DSMEM push (local length <= 4096), 2 chunked through L2  */
+                                 DSMEM push (local length <= 4096), 2 chunked through L2,
+                                 3 multi-pass (local length > 8192: R x S rows through the
+                                 global apply buffer, then chunked through L2)              */
   int32_t chunk;              /* exchange 2: column pairs per chunk                     */
   int32_t vsmem;              /* 1: Krylov vectors kept in shared memory, 0: in HBM     */
   int32_t resident;           /* 1: per-level multiplier/twiddle tables in shared memory*/

@@ -70,6 +70,9 @@ def lib():
             "orc_exact": (C.c_int, [pp, d, pd]),
             "orc_ge_solve": (C.c_int, [i64, pd, pd]),
             "orc_matvec": (C.c_int, [pp, i64, C.c_int, pd, pd]),
+            "orc_matvec_rows": (C.c_int, [pp, i64, C.c_int, pd, C.POINTER(C.c_int64), i64, pd]),
+            "orc_generator": (C.c_int, [pp, i64, C.c_int, pd, pd]),
+            "orc_rhs_rows": (C.c_int, [pp, i64, pd, C.POINTER(C.c_int64), i64, pd]),
             "orc_rhs_nodense": (C.c_int, [pp, i64, pd, pd]),
             "orc_solve": (C.c_int, [pp, pd]),
             "orc_solve_level": (C.c_int, [pp, i64, pd, pd]),
@@ -201,6 +204,36 @@ def matvec(p: Problem, j: int, which: int, x: np.ndarray) -> np.ndarray:
     cp = p.c()
     assert lib().orc_matvec(C.byref(cp), j, which, _pd(x), _pd(y)) == 0
     return y
+
+
+def matvec_rows(p: Problem, j: int, which: int, x: np.ndarray, rows) -> np.ndarray:
+    """Rows `rows` of A x (which=0) / B x (which=1): the literal row sums of matvec, O(n) each."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    y = np.zeros(len(rows))
+    cp = p.c()
+    assert lib().orc_matvec_rows(C.byref(cp), j, which, _pd(x),
+                                 rows.ctypes.data_as(C.POINTER(C.c_int64)), len(rows), _pd(y)) == 0
+    return y
+
+
+def rhs_rows(p: Problem, j: int, U: np.ndarray, rows) -> np.ndarray:
+    """Rows `rows` of the level-j RHS from the history U[0..j] (same arithmetic as rhs_nodense)."""
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    g = np.zeros(len(rows))
+    cp = p.c()
+    assert lib().orc_rhs_rows(C.byref(cp), j, _pd(U), rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                              len(rows), _pd(g)) == 0
+    return g
+
+
+def generator(p: Problem, j: int, which: int):
+    """Toeplitz generator (first column, first row) of A (which=0) / B (which=1) at level j."""
+    col, row = np.zeros(p.n), np.zeros(p.n)
+    cp = p.c()
+    assert lib().orc_generator(C.byref(cp), j, which, _pd(col), _pd(row)) == 0
+    return col, row
 
 
 def rhs_nodense(p: Problem, j: int, U: np.ndarray) -> np.ndarray:

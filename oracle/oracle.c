@@ -344,32 +344,75 @@ int orc_rhs(const orc_problem *p, int64_t j, const double *U, double *g) {
  * accumulated in x87 extended precision, as the refinement residuals are (R-refine): at
  * n = 2^17 the entries reach h^{-beta} ~ 1e10 and cancel to O(1), so a double accumulator
  * would add its own ~1e-6 relative error to a residual check of that size.              */
-int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y) {
-  if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
+/* Level-j scalars of the literal operator (eq3.3): A = eta I - sigma L, B = eta I +
+ * (1 - sigma) L, L = gamma/(2h) Q + d+/h^beta W + d-/h^beta W^T, with omega the WSGD weights. */
+typedef struct { double eta, mu, q, dph, dmh; int64_t n; double *omega; } mv_ctx;
+
+static int mv_setup(const orc_problem *p, int64_t j, int which, mv_ctx *c) {
+  if (!grid_ok(p) || j < 0 || j >= p->M || (which != 0 && which != 1)) return -1;
   const int64_t n = p->n;
   const double h = (p->b - p->a) / (double)(n + 1);
   const double tau = p->T / (double)p->M;
   const double sigma = 1.0 - p->alpha / 2.0;
   const double t = ((double)j + sigma) * tau;
-  const double gam = orc_eval_fn(p->gamma, t);
-  const double dp = orc_eval_fn(p->dplus, t), dm = orc_eval_fn(p->dminus, t);
   const double hb = pow(h, p->beta);
-  const double eta = orc_eta(p->alpha, tau, j);
-  const double mu = (which == 0) ? -sigma : (1.0 - sigma);
-  double *omega = (double *)malloc(sizeof(double) * (size_t)(n + 2));
-  orc_wsgd(p->beta, n + 1, omega);
+  c->n = n;
+  c->eta = orc_eta(p->alpha, tau, j);
+  c->mu = (which == 0) ? -sigma : (1.0 - sigma);
+  c->q = orc_eval_fn(p->gamma, t) / (2.0 * h);
+  c->dph = orc_eval_fn(p->dplus, t) / hb;
+  c->dmh = orc_eval_fn(p->dminus, t) / hb;
+  c->omega = (double *)malloc(sizeof(double) * (size_t)(n + 2));
+  orc_wsgd(p->beta, n + 1, c->omega);
+  return 0;
+}
+
+/* L[i][m] written out: W[i][m] = omega_{i-m+1}, W^T[i][m] = omega_{m-i+1} (zero for negative
+ * index), Q[i][i+1] = 1, Q[i][i-1] = -1 (central difference of the convection term). */
+static double mv_L(const mv_ctx *c, int64_t i, int64_t m) {
+  const double W = (i - m + 1 >= 0) ? c->omega[i - m + 1] : 0.0;
+  const double WT = (m - i + 1 >= 0) ? c->omega[m - i + 1] : 0.0;
+  const double Q = (m == i + 1) ? 1.0 : ((m == i - 1) ? -1.0 : 0.0);
+  return c->q * Q + c->dph * W + c->dmh * WT;
+}
+
+/* row i of the product, the row sum in extended precision (reading R-refine) */
+static double mv_row(const mv_ctx *c, int64_t i, const double *x) {
+  long double s = 0.0L;
+  for (int64_t m = 0; m < c->n; ++m) s += (long double)mv_L(c, i, m) * (long double)x[m];
+  return (double)((long double)c->eta * (long double)x[i] + (long double)c->mu * s);
+}
+
+int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y) {
+  mv_ctx c;
+  if (mv_setup(p, j, which, &c)) return -1;
+  const int64_t n = c.n;
 #pragma omp parallel for schedule(static) if (n > 256)
-  for (int64_t i = 0; i < n; ++i) {
-    long double s = 0.0L;
-    for (int64_t m = 0; m < n; ++m) {
-      double W = (i - m + 1 >= 0) ? omega[i - m + 1] : 0.0;
-      double WT = (m - i + 1 >= 0) ? omega[m - i + 1] : 0.0;
-      double Q = (m == i + 1) ? 1.0 : ((m == i - 1) ? -1.0 : 0.0);
-      s += (long double)(gam / (2.0 * h) * Q + dp / hb * W + dm / hb * WT) * (long double)x[m];
-    }
-    y[i] = (double)((long double)eta * (long double)x[i] + (long double)mu * s);
+  for (int64_t i = 0; i < n; ++i) y[i] = mv_row(&c, i, x);
+  free(c.omega);
+  return 0;
+}
+
+int orc_matvec_rows(const orc_problem *p, int64_t j, int which, const double *x, const int64_t *rows,
+                    int64_t nr, double *y) {
+  mv_ctx c;
+  if (mv_setup(p, j, which, &c)) return -1;
+  for (int64_t k = 0; k < nr; ++k)
+    if (rows[k] < 0 || rows[k] >= c.n) { free(c.omega); return -1; }
+#pragma omp parallel for schedule(static) if (nr > 4)
+  for (int64_t k = 0; k < nr; ++k) y[k] = mv_row(&c, rows[k], x);
+  free(c.omega);
+  return 0;
+}
+
+int orc_generator(const orc_problem *p, int64_t j, int which, double *col, double *row) {
+  mv_ctx c;
+  if (mv_setup(p, j, which, &c)) return -1;
+  for (int64_t i = 0; i < c.n; ++i) {
+    col[i] = (i == 0 ? c.eta : 0.0) + c.mu * mv_L(&c, i, 0);
+    row[i] = (i == 0 ? c.eta : 0.0) + c.mu * mv_L(&c, 0, i);
   }
-  free(omega);
+  free(c.omega);
   return 0;
 }
 
@@ -393,6 +436,32 @@ int orc_rhs_nodense(const orc_problem *p, int64_t j, const double *U, double *g)
   double *f = (double *)malloc(sizeof(double) * (size_t)n);
   orc_source(p, j, ((double)j + sigma) * tau, f);
   for (int64_t i = 0; i < n; ++i) g[i] += f[i];
+  free(f);
+  return 0;
+}
+
+/* Rows rows[0..nr) of the same RHS (alg1 step 2, eq3.1): B u^j - kappa sum_{s<j} c_{j-s}
+ * (u^{s+1} - u^s) + f^{j+sigma}, each row O(n + j). */
+int orc_rhs_rows(const orc_problem *p, int64_t j, const double *U, const int64_t *rows, int64_t nr,
+                 double *g) {
+  if (!grid_ok(p) || j < 0 || j >= p->M) return -1;
+  const int64_t n = p->n;
+  const double tau = p->T / (double)p->M;
+  const double sigma = 1.0 - p->alpha / 2.0;
+  const double kappa = pow(tau, -p->alpha) / tgamma(2.0 - p->alpha);
+  if (orc_matvec_rows(p, j, 1, U + j * n, rows, nr, g)) return -1;
+  if (j >= 1) {
+    double *c = (double *)malloc(sizeof(double) * (size_t)(j + 1));
+    orc_c_row(p->alpha, j, c);
+    for (int64_t s = 0; s <= j - 1; ++s) {
+      const double w = kappa * c[j - s];
+      for (int64_t k = 0; k < nr; ++k) g[k] -= w * (U[(s + 1) * n + rows[k]] - U[s * n + rows[k]]);
+    }
+    free(c);
+  }
+  double *f = (double *)malloc(sizeof(double) * (size_t)n);
+  orc_source(p, j, ((double)j + sigma) * tau, f);
+  for (int64_t k = 0; k < nr; ++k) g[k] += f[rows[k]];
   free(f);
   return 0;
 }

@@ -64,7 +64,15 @@ int orc_exact(const orc_problem *p, double t, double *u);
 int orc_ge_solve(int64_t n, double *A, double *x_inout);
 /* Matrix-free A (which=0) / B (which=1) product and RHS for large n (O(n) memory). */
 int orc_matvec(const orc_problem *p, int64_t j, int which, const double *x, double *y);
+/* The same product at the rows rows[0..nr) only: y[k] = (A x)[rows[k]] (O(n) per row). */
+int orc_matvec_rows(const orc_problem *p, int64_t j, int which, const double *x, const int64_t *rows,
+                    int64_t nr, double *y);
+/* Toeplitz generator of A (which=0) / B (which=1): col[i] = M[i][0], row[m] = M[0][m]. */
+int orc_generator(const orc_problem *p, int64_t j, int which, double *col, double *row);
 int orc_rhs_nodense(const orc_problem *p, int64_t j, const double *U, double *g);
+/* Rows rows[0..nr) of the same RHS (same arithmetic order per row). */
+int orc_rhs_rows(const orc_problem *p, int64_t j, const double *U, const int64_t *rows, int64_t nr,
+                 double *g);
 /* Full IDS run (alg1) with a direct solve per level: U[(M+1)][n]. */
 int orc_solve(const orc_problem *p, double *U);
 /* Same, but solve level j only from a given history (teacher forcing): out[n]. */

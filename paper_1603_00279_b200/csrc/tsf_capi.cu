@@ -442,7 +442,7 @@ int tsf_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, tsf_plan_info
     info->embed_len = pl.n;
     info->precond_len = pl.n / 2;
     info->workspace_bytes = pl.total;
-    info->exchange = pl.C == 1 ? 0 : (pl.staged ? 1 : 2);
+    info->exchange = pl.C == 1 ? 0 : (pl.staged ? 1 : (pl.big ? 3 : 2));
     info->chunk = pl.chunk;
     info->vsmem = pl.vsmem;
     info->resident = pl.resident;
@@ -799,7 +799,7 @@ int tsf_handle_info(const tsf_handle *h, tsf_plan_info *info) {
   info->embed_len = h->pl.n;
   info->precond_len = h->pl.n / 2;
   info->workspace_bytes = h->pl.total;
-  info->exchange = h->pl.C == 1 ? 0 : (h->pl.staged ? 1 : 2);
+  info->exchange = h->pl.C == 1 ? 0 : (h->pl.staged ? 1 : (h->pl.big ? 3 : 2));
   info->chunk = h->pl.chunk;
   info->vsmem = h->pl.vsmem;
   info->resident = h->pl.resident;

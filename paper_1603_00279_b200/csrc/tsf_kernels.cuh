@@ -68,6 +68,7 @@ struct Inst {
   double2 *mul;          // per-level multiplier tables [n + n/2] (task order), HBM variant
   double2 *gsf;          // NEXT-2: spectra of the 4 triangular GSF factors [4][n+1] (task order)
   double2 *xg;           // unstaged clusters: L2 exchange buffer [C][L1e] of the local FFT outputs
+  double2 *xa;           // multi-pass regime: apply input/output buffer [C][L1e] (natural local order)
   const double *phi;     // u^0 (permuted chunks)
   const double *fdev;    // borrowed device source table (natural order) or nullptr
   int32_t *it, *st;
@@ -92,6 +93,7 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.mul = reinterpret_cast<double2 *>(base + P.o_mul);
   I.gsf = reinterpret_cast<double2 *>(base + P.o_gsf);
   I.xg = reinterpret_cast<double2 *>(base + P.o_xg);
+  I.xa = reinterpret_cast<double2 *>(base + P.o_xa);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
   I.trr = reinterpret_cast<double *>(base + P.o_trr);
@@ -255,7 +257,8 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   s.fuse_min = fuse_min;
   s.chunk = chunk;
   double2 *c = reinterpret_cast<double2 *>(raw);
-  s.A = c; c += L1e + kPadBuf * (L1e / 16);
+  const int la = L1e > kMaxLocal ? kMaxLocal : L1e;   // one row in the multi-pass regime
+  s.A = c; c += la + kPadBuf * (la / 16);
   if (staged) { s.B = c; c += L1e; s.O = c; c += L1e + kPadBuf * (L1e / 16); }
   else if (chunk > 0) { s.B = c; c += 5 * chunk * C; }   // chunk buffer [2 chunk C] + 3 prefetched tables
   if (resident) {
@@ -819,6 +822,7 @@ __device__ __forceinline__ void pair_self(double2 &Z, double2 la, double2 lb, do
 struct Geo {
   int L1, L, np, twL, tw2L;   // twL = twN/L (W_L factor), tw2L = twN/(2L)
   int l1;                     // log2(L1)
+  int lr, ls;                 // multi-pass regime: L1 = R x S, lr = log2 R, ls = log2 S (else 0, l1)
   int lnp;                    // log2(np): task indices split by shifts, not integer division
   const int32_t *slot;
   const double2 *ctw;         // resident column twiddles W_L^{q k1(col)} [q ncol + col]
@@ -859,6 +863,13 @@ __device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col) {
   const int pi = int(r) + (col >> 1) * C;
   if (pi == 0) return (col & 1) ? L1 / 2 : 0;
   return (col & 1) ? L1 - pi : pi;
+}
+
+// Slot of local bin k1 in a CTA's staged transform output (xg row): the SMEM DIF FFT puts bin k
+// in slot dslot(k); in the multi-pass regime row rho' = k1 mod R holds the S-point spectrum of
+// bins rho' + R k (see apply_big), so k1 sits at rho' S + dslot(k1 / R).
+__device__ __forceinline__ int gslot(const Geo &g, int k1) {
+  return ((k1 & ((1 << g.lr) - 1)) << g.ls) + dslot(k1 >> g.lr, g.ls);
 }
 
 // C > 1, staged: the four-step column stage through the receive buffer B and the output O,
@@ -1011,7 +1022,7 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
                                               const double2 *__restrict__ tw, uint32_t r, const Smem &sm,
                                               double2 *__restrict__ xg) {
   TSF_PT0();
-  const int L1 = g.L1, np = g.np, l1 = g.l1;
+  const int L1 = g.L1, np = g.np;
   const int W = 2 * CP;                       // columns per chunk
   // Every global (L2) access below is latency bound (~600-900 cycles per dependent round trip):
   // each thread issues a batch of independent loads before using any of them (memory-level
@@ -1027,7 +1038,7 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
     for (int u = threadIdx.x; u < tot; u += kThreads) {
       const int q = u / (2 * cp), col = u - q * (2 * cp);
       const int k1 = col_k1(L1, C, r, 2 * c0 + col);
-      cp_async16(Bc + q * W + col, xg + q * L1 + dslot(k1, l1));
+      cp_async16(Bc + q * W + col, xg + q * L1 + gslot(g, k1));
     }
     // the bin-pair stage's multipliers (task-order table, contiguous in i) and split twiddles,
     // prefetched with the pull so their L2 latency overlaps it
@@ -1150,13 +1161,94 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
       for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], wq[q]);
       // back into the L2 staging rows, in place: the slots of a column pair are read and written
       // only by the pair's owner (L2 stores run at ~10x the per-SM rate of DSMEM stores)
-      const int sl = dslot(k1, l1);
+      const int sl = gslot(g, k1);
 #pragma unroll
       for (int q = 0; q < C; ++q) __stcg(xg + q * L1 + sl, z[q]);
     }
     __syncthreads();                            // Bc is refilled by the next chunk
     TSF_PACC(sm, PS_COLI);
   }
+}
+
+// ------------------------------------------------------------------------ multi-pass regime
+// n > 2^17 (local transforms of L1 = R x S points, S = kMaxLocal, R = 2..8): the CTA's apply
+// buffer X = xa + r L1e (global, natural local order) replaces the SMEM buffer A.  Forward
+// (m = s + S rho, k1 = rho' + R k):
+//   F1  Y[rho'][s] = W_{L1}^{s rho'} sum_rho x[s + S rho] W_R^{rho rho'}   (R-point DFTs, in place)
+//   F2  row rho' -> SMEM, S-point DIF FFT, staged into xg at row rho' (slot p holds bin
+//       rho' + R dperm(p), gslot), then the chunked column stage of the cluster (cross_chunked);
+// inverse: I2 row rho' of xg -> SMEM, S-point DIT FFT, times conj W_{L1}^{s rho'} back into X;
+//   I1  inverse R-point DFTs over stride S.  Every element of X is read and written by the same
+// thread in F1, F2's copies, I2's stores and I1 (S is a multiple of kThreads), and the vector
+// loops touch element e from thread e mod kThreads too, so only SMEM reuse needs barriers.
+template <int R, bool INV>
+__device__ __forceinline__ void rows_dft(double2 *__restrict__ X, int S, const Smem &sm, int tf) {
+  for (int s = threadIdx.x; s < S; s += kThreads) {
+    double2 x[R];
+    if (!INV) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q] = X[s + q * S];
+      fft_reg<R, false>(x);
+#pragma unroll
+      for (int q = 0; q < R; ++q) X[q * S + s] = q ? cmul(x[q], twid(sm, s * q * tf)) : x[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q] = X[q * S + s];
+      fft_reg<R, true>(x);
+#pragma unroll
+      for (int q = 0; q < R; ++q) X[s + q * S] = x[q];
+    }
+  }
+}
+template <bool INV>
+__device__ __forceinline__ void rows_dft_any(double2 *X, int lr, int S, const Smem &sm, int tf) {
+  if (lr == 1) rows_dft<2, INV>(X, S, sm, tf);
+  else if (lr == 2) rows_dft<4, INV>(X, S, sm, tf);
+  else if (lr == 3) rows_dft<8, INV>(X, S, sm, tf);
+}
+
+template <int C>
+__device__ __noinline__ double2 *apply_big(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                           const double2 *__restrict__ tw, uint32_t r,
+                                           double2 *__restrict__ xg, double2 *__restrict__ xa) {
+  TSF_PT0();
+  const int L1 = g.L1, R = 1 << g.lr, S = 1 << g.ls;
+  const int tf = L1e / L1;                    // W_{L1}^x = W_{L1e}^{x tf}
+  double2 *X = xa + int64_t(r) * L1e;
+  double2 *xr = xg + int64_t(r) * L1;
+  if (R > 1) rows_dft_any<false>(X, g.lr, S, sm, tf);       // F1 (same-thread elements)
+  for (int rho = 0; rho < R; ++rho) {                        // F2
+    for (int p = threadIdx.x; p < S; p += kThreads) cp_async16(sm.A + pidx(p), X + rho * S + p);
+    cp_async_wait_all();
+    __syncthreads();
+    local_fft<false>(sm.A, S, sm, L1e);
+    for (int p = threadIdx.x; p < S; p += kThreads) __stcg(xr + rho * S + p, sm.A[pidx(p)]);
+    __syncthreads();                          // A is refilled by the next row
+  }
+  TSF_PACC(sm, PS_FFT_F);
+  csync<C>();                                 // every row of every CTA staged in L2
+  TSF_PACC(sm, PS_BAR1);
+  cross_chunked<C>(sm.A, sm.B, sm.chunk, g, op, tw, r, sm, xg);
+  TSF_PTR();
+  csync<C>();                                 // every column result back in L2
+  TSF_PACC(sm, PS_BAR3);
+  for (int rho = 0; rho < R; ++rho) {                        // I2
+    for (int p = threadIdx.x; p < S; p += kThreads) cp_async16(sm.A + pidx(p), xr + rho * S + p);
+    cp_async_wait_all();
+    __syncthreads();
+    local_fft<true>(sm.A, S, sm, L1e);
+    for (int s = threadIdx.x; s < S; s += kThreads) {
+      const double2 v = sm.A[pidx(s)];
+      X[rho * S + s] = rho ? cmulc(v, twid(sm, s * rho * tf)) : v;
+    }
+    __syncthreads();
+  }
+  if (R > 1) rows_dft_any<true>(X, g.lr, S, sm, tf);        // I1
+  TSF_PACC(sm, PS_FFT_I);
+#ifdef TSF_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
+#endif
+  return X;
 }
 
 // y = op(x) for the CTA's local data already in A[0..L1) (natural order, visible).
@@ -1170,9 +1262,9 @@ __device__ __forceinline__ void cross_chunked(double2 *A, double2 *Bc, int CP, c
 #define TSF_APPLY_ATTR __forceinline__
 #endif
 template <int C, bool STG>
-__device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
-                                       const double2 *__restrict__ tw, uint32_t r, Xch &xs,
-                                       double2 *xg = nullptr) {
+__device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                            const double2 *__restrict__ tw, uint32_t r, Xch &xs,
+                                            double2 *xg) {
   TSF_PT0();
   local_fft<false>(sm.A, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_F);
@@ -1211,6 +1303,15 @@ __device__ TSF_APPLY_ATTR double2 *apply(const Smem &sm, int L1e, const Geo &g, 
   return Y;
 }
 
+// Operator application: the SMEM four-step (n <= 2^17) or the multi-pass regime (BIG).
+template <int C, bool STG, bool BIG = false>
+__device__ __forceinline__ double2 *apply(const Smem &sm, int L1e, const Geo &g, const SpecOp &op,
+                                         const double2 *__restrict__ tw, uint32_t r, Xch &xs,
+                                         double2 *xg = nullptr, double2 *xa = nullptr) {
+  if constexpr (BIG) return apply_big<C>(sm, L1e, g, op, tw, r, xg, xa);
+  else return apply_smem<C, STG>(sm, L1e, g, op, tw, r, xs, xg);
+}
+
 // ------------------------------------------------------------------------ operator setup
 enum Which { OP_A = 0, OP_B = 1, OP_AT = 2, OP_PINV = 3, OP_PTINV = 4 };
 
@@ -1221,6 +1322,8 @@ __device__ __forceinline__ Geo geo_embed(const DevParams &P, const Smem &sm) {
   g.ctw = sm.ctwe;
   g.l1 = __ffs(g.L1) - 1;
   g.lnp = __ffs(g.np) - 1;
+  g.lr = P.lre;
+  g.ls = g.l1 - g.lr;
   return g;
 }
 __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
@@ -1230,6 +1333,8 @@ __device__ __forceinline__ Geo geo_prec(const DevParams &P, const Smem &sm) {
   g.ctw = sm.ctwp;
   g.l1 = __ffs(g.L1) - 1;
   g.lnp = __ffs(g.np) - 1;
+  g.lr = P.lrp;
+  g.ls = g.l1 - g.lr;
   return g;
 }
 
@@ -1327,6 +1432,23 @@ __device__ __forceinline__ SpecOp make_gsf_op(const DevParams &P, const Inst &I,
   return op;
 }
 
+// ------------------------------------------------------------------------ apply buffer view
+// The operator input/output of this CTA, element e of the local chunk: the swizzled SMEM buffer
+// (A, or O in the staged mode), or in the multi-pass regime the global apply buffer (linear).
+template <bool BIG>
+struct ABuf {
+  double2 *p;
+  __device__ __forceinline__ double2 &operator[](int e) const {
+    if constexpr (BIG) return p[e];
+    else return p[pidx(e)];
+  }
+};
+template <bool BIG>
+__device__ __forceinline__ ABuf<BIG> abuf_in(const DevParams &P, const Inst &I, const Smem &sm, uint32_t r) {
+  if constexpr (BIG) return ABuf<BIG>{I.xa + int64_t(r) * P.L1e};
+  else return ABuf<BIG>{sm.A};
+}
+
 // ------------------------------------------------------------------------ vector storage
 // Krylov vectors of this CTA's chunk (npc = L1p complex values): SMEM slots when the plan
 // keeps them on chip (P.vsmem), else the instance's HBM vector block (permuted chunks).
@@ -1384,13 +1506,14 @@ struct T5 { double2 a, b, c, d, f; };
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
 // First half: the memory term into Hsum and u^j (zero-padded) into A; the caller applies B.
-template <int C>
+template <int C, bool BIG>
 __device__ __forceinline__ void rhs_pre(const DevParams &P, const Smem &sm, const Inst &I, int64_t j, uint32_t r,
                                         const double2 *U, double2 *Hsum, bool use_pre) {
   // (use_pre is dropped below when the helpers do not deliver in time)
   const int npc = P.L1p;
   const int64_t n = P.n;
   TSF_PT0();
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);
   const double2 *H = reinterpret_cast<const double2 *>(I.hist) + r * npc;
   const int64_t hstride = n / 2;  // double2 per history row
   // history term kappa (e_j d^0 + sum_{s=1}^{j-1} chat_{j-s} d^s) into Hs (the X slot, zeroed after
@@ -1466,21 +1589,23 @@ __device__ __forceinline__ void rhs_pre(const DevParams &P, const Smem &sm, cons
   }
   TSF_PACC(sm, PS_RHS_HIST);
   TSF_FOR_E(npc) {
-    sm.A[pidx(e)] = U[e];
-    sm.A[pidx(e + npc)] = zero2();
+    AX[e] = U[e];
+    AX[e + npc] = zero2();
   }
 }
 
 // Second half of the RHS: g = Y - Hs + f from the product Y = B u^j; g into A[0..npc)
 // (A[npc..2npc) zero).  Returns the local partial ||g||^2.
+template <bool BIG>
 __device__ __forceinline__ double rhs_post(const DevParams &P, const Smem &sm, const Inst &I, int64_t j,
-                                           uint32_t r, const double2 *Y, const double2 *Hs) {
+                                           uint32_t r, const ABuf<BIG> Y, const double2 *Hs) {
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);
   const int npc = P.L1p;
   const int64_t n = P.n, hstride = n / 2;
   const int C = P.C;
   double acc = 0.0;
   TSF_FOR_E(npc) {
-    double2 g = Y[pidx(e)];
+    double2 g = Y[e];
     if (j >= 1) g = csub(g, Hs[e]);
     if (P.src_kind == TSF_SRC_SEPARABLE) {
       const double2 *Bs = reinterpret_cast<const double2 *>(I.basis) + r * npc;
@@ -1494,23 +1619,23 @@ __device__ __forceinline__ double rhs_post(const DevParams &P, const Smem &sm, c
         g = cadd(g, F[j * hstride + e]);
       }
     }
-    sm.A[pidx(e)] = g;
-    sm.A[pidx(e + npc)] = zero2();
+    AX[e] = g;
+    AX[e + npc] = zero2();
     acc += cdot(g, g);
   }
   return acc;
 }
 
 // Whole RHS (debug hook): history, B u^j, g.
-template <int C, bool STG>
+template <int C, bool STG, bool BIG>
 __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, const Inst &I, const Geo &ge,
                                             const SpecOp &opB, int64_t j, uint32_t r, const double2 *U,
                                             double2 *Hsum, Xch &xs) {
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  rhs_pre<C>(P, sm, I, j, r, U, Hsum, false);
+  rhs_pre<C, BIG>(P, sm, I, j, r, U, Hsum, false);
   __syncthreads();
-  const double2 *Y = apply<C, STG>(sm, P.L1e, ge, opB, tw, r, xs, I.xg);
-  return rhs_post(P, sm, I, j, r, Y, Hsum);
+  const ABuf<BIG> Y{apply<C, STG, BIG>(sm, P.L1e, ge, opB, tw, r, xs, I.xg, I.xa)};
+  return rhs_post<BIG>(P, sm, I, j, r, Y, Hsum);
 }
 
 // ------------------------------------------------------------------------ one level
@@ -1521,7 +1646,7 @@ __device__ __forceinline__ double rhs_phase(const DevParams &P, const Smem &sm, 
 // each factor applied through its 2n circulant embedding (four fused FFT applications), then
 // the true residual ||A u - g|| / ||g|| (one more application) is stored as the level's relres.
 // g arrives in A[0..npc) (rhs_phase) with ||g||^2 local partial g2loc.
-template <int C, bool STG>
+template <int C, bool STG, bool BIG>
 __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
                                           int64_t j, uint32_t r, Xch &xs, double g2loc) {
   const int npc = P.L1p;
@@ -1529,50 +1654,51 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
   const Geo ge = geo_embed(P, sm);
   double2 *G = V.R, *Z1 = V.S, *Z2 = V.PH, *X = V.X;
-  TSF_FOR_E(npc) { G[e] = sm.A[pidx(e)]; }
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);
+  ABuf<BIG> Y = AX;
+  TSF_FOR_E(npc) { G[e] = AX[e]; }
   double g2[1] = {g2loc};
   csum<C, 1>(g2, sm, xs);
   const double inv_xi0 = I.par[7];
-  const double2 *Y;
   // z1 = R_p^0 g, z2 = R_p g
   for (int k = 0; k < 2; ++k) {
     TSF_FOR_E(npc) {
-      sm.A[pidx(e)] = G[e];
-      sm.A[pidx(e + npc)] = zero2();
+      AX[e] = G[e];
+      AX[e + npc] = zero2();
     }
     __syncthreads();
     const SpecOp op = make_gsf_op(P, I, k, r, sm);
-    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
+    Y.p = apply<C, STG, BIG>(sm, P.L1e, ge, op, tw, r, xs, I.xg, I.xa);
     double2 *Z = k == 0 ? Z1 : Z2;
-    TSF_FOR_E(npc) { Z[e] = Y[pidx(e)]; }
+    TSF_FOR_E(npc) { Z[e] = Y[e]; }
   }
   // z3 = L_p^0 z1 (kept in X), z4 = L_p z2, u = (z4 - z3) / xi_0
   for (int k = 2; k < 4; ++k) {
     const double2 *Z = k == 2 ? Z1 : Z2;
     TSF_FOR_E(npc) {
-      sm.A[pidx(e)] = Z[e];
-      sm.A[pidx(e + npc)] = zero2();
+      AX[e] = Z[e];
+      AX[e + npc] = zero2();
     }
     __syncthreads();
     const SpecOp op = make_gsf_op(P, I, k, r, sm);
-    Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
+    Y.p = apply<C, STG, BIG>(sm, P.L1e, ge, op, tw, r, xs, I.xg, I.xa);
     if (k == 2) {
-      TSF_FOR_E(npc) { X[e] = Y[pidx(e)]; }
+      TSF_FOR_E(npc) { X[e] = Y[e]; }
     } else {
-      TSF_FOR_E(npc) { X[e] = cscale(csub(Y[pidx(e)], X[e]), inv_xi0); }
+      TSF_FOR_E(npc) { X[e] = cscale(csub(Y[e], X[e]), inv_xi0); }
     }
   }
   // true residual of the level: ||A u - g|| / ||g||
   TSF_FOR_E(npc) {
-    sm.A[pidx(e)] = X[e];
-    sm.A[pidx(e + npc)] = zero2();
+    AX[e] = X[e];
+    AX[e + npc] = zero2();
   }
   __syncthreads();
   const SpecOp opA = make_op(P, I, j, OP_A, r, sm);
-  Y = apply<C, STG>(sm, P.L1e, ge, opA, tw, r, xs, I.xg);
+  Y.p = apply<C, STG, BIG>(sm, P.L1e, ge, opA, tw, r, xs, I.xg, I.xa);
   double rs[1] = {0.0};
   TSF_FOR_E(npc) {
-    const double2 d = csub(Y[pidx(e)], G[e]);
+    const double2 d = csub(Y[e], G[e]);
     rs[0] += cdot(d, d);
   }
   csum<C, 1>(rs, sm, xs);
@@ -1612,7 +1738,7 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
 // a single state machine for everything cost ~6% at C3 against this shape.
 enum LevelState { S_RHS = 0, S_WARM = 1, S_TRUE = 2, S_KRYLOV = 3 };
 
-template <int C, int METHOD, bool STG>
+template <int C, int METHOD, bool STG, bool BIG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
                                             int64_t j, uint32_t r, Xch &xs, int mode = 0, int64_t j0 = 0) {
   const int npc = P.L1p;
@@ -1633,12 +1759,13 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   const bool tres = P.true_res && mode == 0;
   int hs = 0, status = TSF_LEVEL_OK;
   double relres = 0.0, gg = 0.0, rr0 = 0.0;
-  const double2 *Y = sm.A;       // output buffer of the last operator application
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);   // operator input of this CTA
+  ABuf<BIG> Y = AX;              // output buffer of the last operator application
 
   double g2[1] = {0.0};
   int ph;
   if (mode == 0) {
-    rhs_pre<C>(P, sm, I, j, r, V.U, V.X, P.helpers > 0 && j >= 2 && j >= j0 + 1);
+    rhs_pre<C, BIG>(P, sm, I, j, r, V.U, V.X, P.helpers > 0 && j >= 2 && j >= j0 + 1);
     ph = S_RHS;
   } else {
     // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
@@ -1646,8 +1773,8 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     TSF_FOR_E(npc) {
       const bool hit = (int64_t(r) == m % C) && (int64_t(e) == m / C);
       const double2 g = hit ? (mode == 1 ? make_double2(1.0, 0.0) : make_double2(0.0, 1.0)) : zero2();
-      sm.A[pidx(e)] = g;
-      sm.A[pidx(e + npc)] = zero2();
+      AX[e] = g;
+      AX[e + npc] = zero2();
       R[e] = g;
       G[e] = g;
       if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
@@ -1666,13 +1793,13 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       {
         const SpecOp op = ph == S_RHS ? make_op(P, I, j, OP_B, r, sm) : opA;
         __syncthreads();
-        Y = apply<C, STG>(sm, P.L1e, ge, op, tw, r, xs, I.xg);
+        Y.p = apply<C, STG, BIG>(sm, P.L1e, ge, op, tw, r, xs, I.xg, I.xa);
       }
       if (ph == S_TRUE) {
         // true residual at exit (SURVEY reading c13): ||g - A u^{j+1}|| / ||g||
         double tr[1] = {0.0};
         TSF_FOR_E(npc) {
-          const double2 d = csub(G[e], Y[pidx(e)]);
+          const double2 d = csub(G[e], Y[e]);
           tr[0] += cdot(d, d);
         }
         csum<C, 1>(tr, sm, xs);
@@ -1680,25 +1807,25 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         break;
       }
       if (ph == S_RHS) {
-        g2[0] = rhs_post(P, sm, I, j, r, Y, V.X);
+        g2[0] = rhs_post<BIG>(P, sm, I, j, r, Y, V.X);
         if constexpr (METHOD == TSF_GSF) {
           if (j >= 1) {          // NEXT-2: the level by the Gohberg-Semencul formula
-            gsf_level<C, STG>(P, I, sm, V, j, r, xs, g2[0]);
+            gsf_level<C, STG, BIG>(P, I, sm, V, j, r, xs, g2[0]);
             return;
           }
         }
         if (warm) {
           // NEXT-3 warm start x0 = u^j: r0 = g - A u^j, stop on ||r|| < tol ||g||
           TSF_FOR_E(npc) {
-            G[e] = sm.A[pidx(e)];
-            sm.A[pidx(e)] = V.U[e];
-            sm.A[pidx(e + npc)] = zero2();
+            G[e] = AX[e];
+            AX[e] = V.U[e];
+            AX[e + npc] = zero2();
           }
           ph = S_WARM;
           continue;
         }
         TSF_FOR_E(npc) {
-          const double2 g = sm.A[pidx(e)];
+          const double2 g = AX[e];
           R[e] = g;
           G[e] = g;
           if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = g; PV[e] = g; }
@@ -1710,7 +1837,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       } else {                   // S_WARM
         double w2[2] = {g2[0], 0.0};
         TSF_FOR_E(npc) {
-          const double2 r0 = csub(G[e], Y[pidx(e)]);
+          const double2 r0 = csub(G[e], Y[e]);
           R[e] = r0;
           if (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF) { RH[e] = r0; PV[e] = r0; }
           if (METHOD == TSF_PCGS) RH[e] = r0;
@@ -1719,8 +1846,8 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         }
         __syncthreads();         // Y may alias A
         TSF_FOR_E(npc) {
-          sm.A[pidx(e)] = R[e];
-          sm.A[pidx(e + npc)] = zero2();
+          AX[e] = R[e];
+          AX[e + npc] = zero2();
         }
         csum<C, 2>(w2, sm, xs);
         gg = w2[0];
@@ -1741,21 +1868,21 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       for (int h = 0;; h = (h + 1) & 3) {
         const bool isP = !(h & 1);
         if (isP && !prec) {
-          Y = sm.A;
+          Y = AX;
         } else {
           __syncthreads();
           const SpecOp op = isP ? opP : opA;
           const Geo g = isP ? gp : ge;
-          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
+          Y.p = apply<C, STG, BIG>(sm, P.L1e, g, op, tw, r, xs, I.xg, I.xa);
         }
         if (isP) {
           // h = 0: phat = Y; h = 2: shat = Y.  Either becomes the (padded) input of A.
           double2 *const Dst = h == 0 ? PH : SH;
           TSF_FOR_E(npc) {
-            const double2 z = Y[pidx(e)];
+            const double2 z = Y[e];
             Dst[e] = z;
-            sm.A[pidx(e)] = z;
-            sm.A[pidx(e + npc)] = zero2();
+            AX[e] = z;
+            AX[e + npc] = zero2();
           }
           continue;
         }
@@ -1763,7 +1890,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
           // v = Y; alpha = rho / (r^.v); s = r - alpha v; half-step exit on ||s||
           double d[1] = {0.0};
           TSF_FOR_E(npc) {
-            const double2 v = Y[pidx(e)];
+            const double2 v = Y[e];
             VV[e] = v;
             d[0] += cdot(RH[e], v);
           }
@@ -1774,7 +1901,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
           TSF_FOR_E(npc) {
             const double2 sv = caxpy(-alpha, VV[e], R[e]);
             S[e] = sv;
-            sm.A[pidx(e)] = sv;
+            AX[e] = sv;
             ss[0] += cdot(sv, sv);
           }
           csum<C, 1>(ss, sm, xs);
@@ -1789,7 +1916,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         // h == 3: t = Y; omega = t.s / t.t; x += alpha phat + omega shat; r = s - omega t
         double tt[2] = {0.0, 0.0};
         TSF_FOR_E(npc) {
-          const double2 t = Y[pidx(e)];
+          const double2 t = Y[e];
           const double2 sv = S[e];
           tt[0] += cdot(t, sv);
           tt[1] += cdot(t, t);
@@ -1800,7 +1927,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         double rr[2] = {0.0, 0.0};
         TSF_FOR_E(npc) {
           X[e] = caxpy(omega, SH[e], caxpy(alpha, PH[e], X[e]));
-          const double2 rn = caxpy(-omega, Y[pidx(e)], S[e]);
+          const double2 rn = caxpy(-omega, Y[e], S[e]);
           R[e] = rn;
           rr[0] += cdot(RH[e], rn);
           rr[1] += cdot(rn, rn);
@@ -1818,7 +1945,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
         TSF_FOR_E(npc) {
           const double2 pv = caxpy(beta, caxpy(-omega, VV[e], PV[e]), R[e]);
           PV[e] = pv;
-          sm.A[pidx(e)] = pv;
+          AX[e] = pv;
         }
       }
     } else if (iterate && METHOD == TSF_PCGS) {
@@ -1837,49 +1964,49 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       for (int h = 0;; h = (h + 1) & 3) {
         const bool isP = !(h & 1);
         if (isP && !prec) {
-          Y = sm.A;
+          Y = AX;
         } else {
           __syncthreads();
           const SpecOp op = isP ? opP : opA;
           const Geo g = isP ? gp : ge;
-          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
+          Y.p = apply<C, STG, BIG>(sm, P.L1e, g, op, tw, r, xs, I.xg, I.xa);
         }
         if (h == 0) {                            // phat
           TSF_FOR_E(npc) {
-            const double2 phv = Y[pidx(e)];
+            const double2 phv = Y[e];
             PH[e] = phv;
-            sm.A[pidx(e)] = phv;
-            sm.A[pidx(e + npc)] = zero2();
+            AX[e] = phv;
+            AX[e + npc] = zero2();
           }
           continue;
         }
         if (h == 1) {                            // vhat: alpha, q = u - alpha vhat, A <- u + q
           double sg[1] = {0.0};
-          TSF_FOR_E(npc) { sg[0] += cdot(RH[e], Y[pidx(e)]); }
+          TSF_FOR_E(npc) { sg[0] += cdot(RH[e], Y[e]); }
           csum<C, 1>(sg, sm, xs);
           if (!(fabs(sg[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
           alpha = rho / sg[0];
           TSF_FOR_E(npc) {                       // Y may alias A: read before the write
             const double2 u = S[e];
-            const double2 q = caxpy(-alpha, Y[pidx(e)], u);
+            const double2 q = caxpy(-alpha, Y[e], u);
             VV[e] = q;
-            sm.A[pidx(e)] = cadd(u, q);
+            AX[e] = cadd(u, q);
           }
           continue;
         }
         if (h == 2) {                            // uhat: x += alpha uhat, A <- uhat
           TSF_FOR_E(npc) {
-            const double2 uh = Y[pidx(e)];
+            const double2 uh = Y[e];
             X[e] = caxpy(alpha, uh, X[e]);
-            sm.A[pidx(e)] = uh;
-            sm.A[pidx(e + npc)] = zero2();
+            AX[e] = uh;
+            AX[e + npc] = zero2();
           }
           continue;
         }
         // h == 3: A uhat: r -= alpha A uhat; rho' = rt.r; ||r||
         double rr[2] = {0.0, 0.0};
         TSF_FOR_E(npc) {
-          const double2 rn = caxpy(-alpha, Y[pidx(e)], R[e]);
+          const double2 rn = caxpy(-alpha, Y[e], R[e]);
           R[e] = rn;
           rr[0] += cdot(RH[e], rn);
           rr[1] += cdot(rn, rn);
@@ -1899,7 +2026,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
           const double2 pv = caxpy(beta, caxpy(beta, PV[e], q), u);
           S[e] = u;
           PV[e] = pv;
-          sm.A[pidx(e)] = pv;
+          AX[e] = pv;
         }
       }
     } else if (iterate && METHOD == TSF_CGNR) {
@@ -1915,54 +2042,54 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       for (int h = 2;; h = (h + 1) & 3) {
         const bool isPre = h == 0 || h == 3;
         if (isPre && !prec) {
-          Y = sm.A;
+          Y = AX;
         } else {
           __syncthreads();
           const SpecOp op = h == 0 ? opP : (h == 1 ? opA : (h == 2 ? opAT : opPT));
           const Geo g = isPre ? gp : ge;
-          Y = apply<C, STG>(sm, P.L1e, g, op, tw, r, xs, I.xg);
+          Y.p = apply<C, STG, BIG>(sm, P.L1e, g, op, tw, r, xs, I.xg, I.xa);
         }
         if (h == 2) {                            // A^T r -> first npc values into A for P^{-T}
-          TSF_FOR_E(npc) { sm.A[pidx(e)] = Y[pidx(e)]; }
+          TSF_FOR_E(npc) { AX[e] = Y[e]; }
           continue;
         }
         if (h == 3) {                            // z = P^{-T} A^T r; gamma, beta; p = z + beta p
           double zz[1] = {0.0};
-          TSF_FOR_E(npc) { zz[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+          TSF_FOR_E(npc) { zz[0] += cdot(Y[e], Y[e]); }
           csum<C, 1>(zz, sm, xs);
           const double beta = first ? 0.0 : zz[0] / gam;
           gam = zz[0];
           TSF_FOR_E(npc) {
-            const double2 z = Y[pidx(e)];
+            const double2 z = Y[e];
             const double2 pv = first ? z : caxpy(beta, PV[e], z);
             PV[e] = pv;
-            sm.A[pidx(e)] = pv;
+            AX[e] = pv;
           }
           first = false;
           continue;
         }
         if (h == 0) {                            // phat
           TSF_FOR_E(npc) {
-            const double2 phv = Y[pidx(e)];
+            const double2 phv = Y[e];
             PH[e] = phv;
-            sm.A[pidx(e)] = phv;
-            sm.A[pidx(e + npc)] = zero2();
+            AX[e] = phv;
+            AX[e + npc] = zero2();
           }
           continue;
         }
         // h == 1: q = A phat; a = gamma / ||q||^2; x += a phat; r -= a q; ||r||
         double qq[1] = {0.0};
-        TSF_FOR_E(npc) { qq[0] += cdot(Y[pidx(e)], Y[pidx(e)]); }
+        TSF_FOR_E(npc) { qq[0] += cdot(Y[e], Y[e]); }
         csum<C, 1>(qq, sm, xs);
         if (!(qq[0] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
         a = gam / qq[0];
         double rl[1] = {0.0};
         TSF_FOR_E(npc) {
           X[e] = caxpy(a, PH[e], X[e]);
-          const double2 rn = caxpy(-a, Y[pidx(e)], R[e]);
+          const double2 rn = caxpy(-a, Y[e], R[e]);
           R[e] = rn;
-          sm.A[pidx(e)] = rn;
-          sm.A[pidx(e + npc)] = zero2();
+          AX[e] = rn;
+          AX[e + npc] = zero2();
           rl[0] += cdot(rn, rn);
         }
         csum<C, 1>(rl, sm, xs);
@@ -1977,8 +2104,8 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     // true residual next, through the cold site: A <- x
     __syncthreads();             // every thread done with the last Y
     TSF_FOR_E(npc) {
-      sm.A[pidx(e)] = X[e];
-      sm.A[pidx(e + npc)] = zero2();
+      AX[e] = X[e];
+      AX[e + npc] = zero2();
     }
     ph = S_TRUE;
   }
@@ -2087,7 +2214,7 @@ __device__ void hist_helper(const DevParams &P, int32_t nlev, int *quit) {
 }
 
 // ------------------------------------------------------------------------ kernels
-template <int C, int METHOD, bool STG, bool VS>
+template <int C, int METHOD, bool STG, bool VS, bool BIG = false>
 __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
     k_solve(DevParams P, int32_t nlev, int32_t mode) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -2118,9 +2245,9 @@ __global__ void __launch_bounds__(kThreads, C == 1 ? TSF_C1_BLOCKS : 1)
   Xch xs;
   const int64_t j0 = *P.level;
   if (mode != 0) {               // NEXT-2 setup solve with the level-1 operators
-    level_solve<C, METHOD, STG>(P, I, sm, V, 1, r, xs, mode);
+    level_solve<C, METHOD, STG, BIG>(P, I, sm, V, 1, r, xs, mode);
   } else {
-    for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG>(P, I, sm, V, j, r, xs, 0, j0);
+    for (int64_t j = j0; j < j0 + nlev && j < P.M; ++j) level_solve<C, METHOD, STG, BIG>(P, I, sm, V, j, r, xs, 0, j0);
   }
   if constexpr (VS) TSF_FOR_E(npc) { Ug[e] = V.U[e]; }
 #ifdef TSF_PROFILE
@@ -2135,7 +2262,7 @@ __global__ void k_advance(int64_t *level, int64_t by, int64_t M);
 // Debug: one operator application of instance b at level j: in/out are permuted chunks.
 // reps > 1 (timing): reps applications alternating P^{-1} and A (as in a Krylov iteration),
 // each feeding the next; out holds the last result.
-template <int C, bool STG>
+template <int C, bool STG, bool BIG = false>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_t reps, int b, int64_t j,
                                                               int which, const double *in, double *out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -2154,27 +2281,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
   const double2 *X = reinterpret_cast<const double2 *>(in) + r * npc;
   double2 *Y = reinterpret_cast<double2 *>(out) + r * npc;
   const double2 *__restrict__ tw = reinterpret_cast<const double2 *>(P.tw);
-  for (int e = threadIdx.x; e < npc; e += kThreads) sm.A[pidx(e)] = X[e];
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);
+  for (int e = threadIdx.x; e < npc; e += kThreads) AX[e] = X[e];
   __syncthreads();
   xinit<C>(sm);
   Xch xs;
   fill_mul(P, I, j, r, sm);
   __syncthreads();
-  const double2 *Z = sm.A;
+  ABuf<BIG> Z = AX;
   const int nrep = reps > 1 ? reps : 1;
   for (int rep = 0; rep < nrep; ++rep) {
     const int wh = reps > 1 ? ((rep & 1) ? OP_A : OP_PINV) : which;
     const bool embed = wh <= OP_AT;
     for (int e = threadIdx.x; e < npc; e += kThreads) {
-      const double2 v = Z[pidx(e)];
-      sm.A[pidx(e)] = v;
-      if (embed) sm.A[pidx(e + npc)] = zero2();
+      const double2 v = Z[e];
+      AX[e] = v;
+      if (embed) AX[e + npc] = zero2();
     }
     __syncthreads();
     const SpecOp op = make_op(P, I, j, wh, r, sm);
-    Z = apply<C, STG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs, I.xg);
+    Z.p = apply<C, STG, BIG>(sm, P.L1e, embed ? geo_embed(P, sm) : geo_prec(P, sm), op, tw, r, xs, I.xg, I.xa);
   }
-  for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[pidx(e)];
+  for (int e = threadIdx.x; e < npc; e += kThreads) Y[e] = Z[e];
 #ifdef TSF_PROFILE
   __syncthreads();
   if (blockIdx.x == TSF_PROF_CTA && threadIdx.x < 32) P.prof[threadIdx.x] += prof_s[threadIdx.x];
@@ -2183,7 +2311,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_apply(DevParams P, int32_
 }
 
 // Debug: RHS of the current level for every instance into V_R.
-template <int C, bool STG>
+template <int C, bool STG, bool BIG = false>
 __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int b = blockIdx.x / C;
@@ -2200,9 +2328,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_debug_rhs(DevParams P, int32_t)
   const SpecOp opB = make_op(P, I, j, OP_B, r, sm);
   const double2 *U = reinterpret_cast<const double2 *>(I.vec + V_U * P.n) + r * npc;
   double2 *Hs = reinterpret_cast<double2 *>(I.vec + V_X * P.n) + r * npc;
-  rhs_phase<C, STG>(P, sm, I, geo_embed(P, sm), opB, j, r, U, Hs, xs);
+  rhs_phase<C, STG, BIG>(P, sm, I, geo_embed(P, sm), opB, j, r, U, Hs, xs);
   double2 *R = reinterpret_cast<double2 *>(I.vec + V_R * P.n) + r * npc;
-  for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = sm.A[pidx(e)];
+  const ABuf<BIG> AX = abuf_in<BIG>(P, I, sm, r);
+  for (int e = threadIdx.x; e < npc; e += kThreads) R[e] = AX[e];
   csync<C>();
 }
 
@@ -2292,11 +2421,37 @@ cudaError_t launch_solve_k(K kern, const Plan &pl, const DevParams &dp0, int32_t
 // tsf_solve_c<C>_m<M>.cu (parallel compilation); launch_solve_c<C> dispatches on the method.
 template <int C, int METHOD>
 cudaError_t launch_solve_cm(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, int32_t mode);
+// Multi-pass regime kernels exist for 16-CTA clusters only.
+template <int CC, int MM, bool ON = (CC == 16)>
+struct BigK {
+  static cudaError_t solve(const Plan &, const DevParams &, int32_t, cudaStream_t, int32_t) {
+    return cudaErrorInvalidValue;
+  }
+  static cudaError_t apply(const Plan &, const DevParams &, int, int64_t, int, const double *, double *,
+                           cudaStream_t, int32_t) {
+    return cudaErrorInvalidValue;
+  }
+  static cudaError_t rhs(const Plan &, const DevParams &, cudaStream_t) { return cudaErrorInvalidValue; }
+};
+template <int CC, int MM>
+struct BigK<CC, MM, true> {
+  static cudaError_t solve(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, int32_t z) {
+    return launch_solve_k(k_solve<CC, MM, false, false, true>, pl, dp, nlev, st, z);
+  }
+  static cudaError_t apply(const Plan &pl, const DevParams &dp, int b, int64_t j, int which, const double *in,
+                           double *out, cudaStream_t st, int32_t reps) {
+    return launch_cluster(k_debug_apply<CC, false, true>, pl, CC, st, dp, reps, b, j, which, in, out);
+  }
+  static cudaError_t rhs(const Plan &pl, const DevParams &dp, cudaStream_t st) {
+    return launch_cluster(k_debug_rhs<CC, false, true>, pl, pl.B * CC, st, dp, int32_t(0));
+  }
+};
 #define TSF_INSTANTIATE_METHOD(CC, MM)                                                          \
   template <>                                                                                   \
   cudaError_t launch_solve_cm<CC, MM>(const Plan &pl, const DevParams &dp, int32_t nlev, cudaStream_t st, \
                                       int32_t z) {                                              \
     constexpr bool S1 = (CC) > 1;                                                               \
+    if (pl.big) return BigK<CC, MM>::solve(pl, dp, nlev, st, z);                                \
     const bool stg = TSF_STG_OF(CC, pl), vs = pl.vsmem != 0;                                    \
     if (stg && vs) return launch_solve_k(k_solve<CC, MM, S1, true>, pl, dp, nlev, st, z);       \
     if (stg) return launch_solve_k(k_solve<CC, MM, S1, false>, pl, dp, nlev, st, z);            \
@@ -2319,12 +2474,14 @@ cudaError_t launch_solve_cm(const Plan &pl, const DevParams &dp, int32_t nlev, c
   cudaError_t launch_dbg_apply_c<CC>(const Plan &pl, const DevParams &dp, int b, int64_t j,     \
                                      int which, const double *in, double *out, cudaStream_t st,  \
                                      int32_t reps) {                                             \
+    if (pl.big) return BigK<CC, 0>::apply(pl, dp, b, j, which, in, out, st, reps);              \
     if (TSF_STG_OF(CC, pl))                                                                     \
       return launch_cluster(k_debug_apply<CC, true>, pl, CC, st, dp, reps, b, j, which, in, out); \
     return launch_cluster(k_debug_apply<CC, false>, pl, CC, st, dp, reps, b, j, which, in, out); \
   }                                                                                             \
   template <>                                                                                   \
   cudaError_t launch_dbg_rhs_c<CC>(const Plan &pl, const DevParams &dp, cudaStream_t st) {      \
+    if (pl.big) return BigK<CC, 0>::rhs(pl, dp, st);                                            \
     if (TSF_STG_OF(CC, pl)) return launch_cluster(k_debug_rhs<CC, true>, pl, pl.B * CC, st, dp, int32_t(0)); \
     return launch_cluster(k_debug_rhs<CC, false>, pl, pl.B * CC, st, dp, int32_t(0));           \
   }

@@ -44,8 +44,8 @@ int sample_points(const tsf_problem &p, double *x, double *t) {
 static int validate_one(const tsf_problem *p) {
   if (!(p->alpha > 0.0 && p->alpha <= 1.0)) return fail("alpha=%g outside (0,1] (P:74)", p->alpha);
   if (!(p->beta > 1.0 && p->beta <= 2.0)) return fail("beta=%g outside (1,2] (P:74)", p->beta);
-  if (!is_pow2(p->n) || p->n < 64 || p->n > 131072)
-    return fail("n=%g must be a power of two in [64, 131072]", double(p->n));
+  if (!is_pow2(p->n) || p->n < 64 || p->n > kMaxN)
+    return fail("n=%g must be a power of two in [64, 1048576]", double(p->n));
   if (p->M < 1) return fail("M=%g must be >= 1", double(p->M));
   if (!(p->b > p->a) || !std::isfinite(p->a) || !std::isfinite(p->b))
     return fail("need a < b (got a=%g, b=%g)", p->a, p->b);
@@ -121,7 +121,8 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
 // every CTA owns >= 1 preconditioner column pair (n >= 4 C^2); for C > 1 one column-pair
 // task per thread (n/(2 C^2) <= 256).
 static bool cluster_ok(int64_t n, int C) {
-  if (n / C > kMaxLocal) return false;
+  // local transforms longer than kMaxLocal: the multi-pass regime, on 16-CTA clusters only
+  if (n / C > kMaxLocal) return C == 16 && n <= kMaxN;
   if (n < 4LL * C * C) return false;
   // C > 1: staged exchange (local length <= 4096) or one column-pair task per thread
   if (C > 1 && n / C > 4096 && n / (2LL * C * C) > kThreads) return false;
@@ -175,12 +176,24 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   if (const char *es = std::getenv("TSF_STAGED")) P.staged = (C > 1) ? std::atoi(es) : 0;
   P.resident = (P.staged && P.L1e <= 1024) ? 1 : 0;
   if (const char *er = std::getenv("TSF_RESIDENT")) P.resident = P.staged ? std::atoi(er) : 0;
+  // multi-pass regime (n > 2^17): each local transform of L1 = R x S points (S <= kMaxLocal)
+  // runs as R-point DFTs over stride S and R SMEM FFTs of S points, through the global apply
+  // buffer; the column stage is the chunked one through L2.  Vectors live in HBM.
+  if (P.L1e > kMaxLocal) {
+    P.big = 1;
+    P.staged = 0;
+    P.resident = 0;
+    auto lg = [](int64_t v) { int l = 0; while ((int64_t(1) << l) < v) ++l; return l; };
+    P.lre = lg(P.L1e / kMaxLocal);
+    P.lrp = P.L1p > kMaxLocal ? lg(P.L1p / kMaxLocal) : 0;
+  }
   // Krylov vectors in SMEM when they fit next to the transform buffers (one CTA per SM for
   // clusters; single-CTA instances keep two CTAs per SM)
   {
     const int64_t with = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, 1);
     P.vsmem = (with <= (C > 1 ? kMaxSmem : kMaxSmem / 2 - 1024)) ? 1 : 0;
     if (const char *ev = std::getenv("TSF_VSMEM")) P.vsmem = (with <= kMaxSmem) ? std::atoi(ev) : 0;
+    if (P.big) P.vsmem = 0;
   }
   P.smem = smem_bytes(P.L1e, P.L1p, P.staged, P.resident, P.vsmem);
   if (C > 1 && !P.staged) {      // chunk buffer [2 chunk C] + 3 prefetched pair tables [chunk C]:
@@ -234,6 +247,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.o_mul = q;   q = up(q + size_t(n + n / 2) * 16);
   P.o_gsf = q;   q = up(q + (s->method == TSF_GSF ? size_t(4) * size_t(n + 1) * 16 : 0));
   P.o_xg = q;    q = up(q + (C > 1 && !P.staged ? size_t(n) * 16 : 0));   // L2 exchange (unstaged)
+  P.o_xa = q;    q = up(q + (P.big ? size_t(n) * 16 : 0));                 // apply buffer (multi-pass)
   P.stride = q;
   P.total = P.off_inst + P.stride * size_t(B);
   *pl = P;
@@ -333,6 +347,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.method = pl.method; d.precond = pl.precond; d.maxit = pl.maxit;
   d.L1e = pl.L1e; d.L1p = pl.L1p; d.npe = pl.npe; d.npp = pl.npp;
   d.staged = pl.staged; d.resident = pl.resident; d.vsmem = pl.vsmem; d.fuse_min = pl.fuse_min; d.chunk = pl.chunk;
+  d.big = pl.big; d.lre = pl.lre; d.lrp = pl.lrp; d.o_xa = pl.o_xa;
   d.tol = pl.tol;
   d.scale_e = 1.0 / (4.0 * double(pl.n));
   d.scale_p = 1.0 / (4.0 * double(pl.n / 2));

@@ -14,7 +14,8 @@
 namespace tsf {
 
 constexpr int kThreads = 256;          // threads per CTA
-constexpr int kMaxLocal = 8192;        // max complex elements of the local FFT (128 KiB)
+constexpr int kMaxLocal = 8192;        // max complex elements of an SMEM-resident local FFT (128 KiB)
+constexpr int64_t kMaxN = 1 << 20;     // largest n (multi-pass regime above n = 2^17)
 constexpr int kNumVec = 13;            // u, Krylov work vectors, phi copy, GSF generators x, y
 constexpr int kSmemVec = 9;            // vectors kept in SMEM when they fit (u, x, r, r^, p, v, s, p^, s^);
                                        // g (read once per level) always lives in HBM
@@ -38,6 +39,9 @@ struct DevParams {
   int32_t vsmem;                   // Krylov vectors in SMEM (else in the instance's HBM block)
   int32_t fuse_min;                // local FFT length from which radix-16 passes are used
   int32_t chunk;                   // column pairs per chunk of the unstaged column stage
+  int32_t big;                     // multi-pass regime: local transforms longer than kMaxLocal
+  int32_t lre, lrp;                // log2 of the row count R = L1 / S of the embedding / preconditioner
+                                   // local transform (S = min(L1, kMaxLocal); 0 unless big)
   double tol;
   double scale_e, scale_p;         // 1/(4L) folding of the real-FFT split and 1/L
   double qscale_p;                 // Lambda_Q scale of the preconditioner: 1 or (n-1)/n
@@ -57,6 +61,7 @@ struct DevParams {
   int64_t stride;                  // bytes between instances
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
   int64_t o_vec, o_hist, o_it, o_rr, o_trr, o_st, o_mul, o_gsf, o_xg, o_phi;
+  int64_t o_xa;                    // multi-pass regime: the apply buffer [C][L1e] (global)
   const double *const *fptr;       // borrowed device f tables (natural order), one per instance
   int32_t ftab_dev;                // 1: the source table is read through fptr
   int32_t x0_warm;                 // NEXT-3: Krylov initial guess u^j (else 0)
@@ -74,6 +79,8 @@ struct Plan {
   int32_t resident = 0; // per-instance constant tables cached in SMEM (small local length)
   int32_t fuse_min = 1024;   // radix-16 passes from L1 = 1024 (measured, tools/fft_ubench.cu)
   int32_t chunk = 0;         // unstaged clusters: column pairs per chunk (chunk buffer 2 chunk C complex)
+  int32_t big = 0;           // multi-pass regime (n / C > kMaxLocal; C = 16): see DESIGN.md
+  int32_t lre = 0, lrp = 0;  // log2 rows of the embedding / preconditioner local transforms
   int64_t smem = 0;
   // workspace layout (byte offsets from the workspace base)
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
@@ -84,6 +91,7 @@ struct Plan {
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;
   int64_t o_vec, o_hist, o_it, o_rr, o_trr, o_st, o_mul, o_gsf, o_xg, o_phi;
+  int64_t o_xa = 0;
   int32_t ftab_dev = 0;      // source table borrowed from device memory (not copied)
 };
 
@@ -146,7 +154,9 @@ DevParams dev_params(const Plan &pl, char *ws);
 // vsmem; 48 doubles of reduction scratch, 128 doubles of pushed CTA partials and 4 mbarriers.
 TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem,
                                  int64_t chunk_cplx = 0) {
-  int64_t c2 = (staged ? 3 * L1e : L1e) + (staged ? 2 : 1) * kPadBuf * (L1e / 16);   // A (+ B, O)
+  // A holds one row of at most kMaxLocal points (multi-pass regime: L1e > kMaxLocal)
+  const int64_t la = L1e > kMaxLocal ? kMaxLocal : L1e;
+  int64_t c2 = (staged ? 3 * la : la) + (staged ? 2 : 1) * kPadBuf * (la / 16);   // A (+ B, O)
   if (resident) c2 += L1e + 3 * (L1e + L1p);      // twiddles, column twiddles, multipliers, pair twiddles
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;

@@ -105,6 +105,25 @@ def test_planner_cluster_choices_and_workspace():
     assert c5.cluster == 16 and c5.smem_bytes <= 227 * 1024
 
 
+@pytest.mark.parametrize("lg", [18, 19, 20])
+def test_planner_multi_pass_regime(lg):
+    """n = 2^18..2^20 (FFT lengths 2^19..2^21 real, north_star): 16-CTA clusters, local
+    transforms of n/16 points as R x 8192 rows (exchange 3), vectors in HBM, SMEM within 227 KiB;
+    n = 2^21 is rejected, and smaller clusters are infeasible (local length > 8192)."""
+    n = 1 << lg
+    inst = Instance(alpha=0.6, beta=1.6, n=n, M=2, gamma=const(0.3), dplus=const(1.0), dminus=const(0.5))
+    pl = tsf.plan([inst])
+    assert (pl.cluster, pl.exchange, pl.vsmem, pl.resident) == (16, 3, 0, 0)
+    assert pl.embed_len == n and pl.precond_len == n // 2
+    assert pl.smem_bytes <= 227 * 1024 and pl.chunk >= 1
+    assert pl.workspace_bytes > (13 + 2 + 2) * n * 8          # vectors, history, apply buffers
+    with pytest.raises(L.TsfError, match="infeasible"):
+        tsf.plan([inst], cluster=8)
+    with pytest.raises(L.TsfError, match="power of two"):
+        tsf.plan([Instance(alpha=0.6, beta=1.6, n=2 * kmax, M=2, gamma=const(0.3), dplus=const(1.0),
+                           dminus=const(0.5))]) if (kmax := 1 << 20) else None
+
+
 def test_init_rejects_small_workspace_without_touching_the_gpu():
     lib = L.load()
     probs, keep = tsf.marshal(CONFIGS["C1"]())

@@ -515,6 +515,35 @@ def test_matrix_free_products_match_delta_operator_and_dense(n, j):
     assert np.linalg.norm(O.matvec(p, j, 0, U[j + 1]) - g) <= 1e-12 * np.linalg.norm(g)
 
 
+@pytest.mark.parametrize("n", [9, 64])
+@pytest.mark.parametrize("j", [0, 3])
+def test_sampled_rows_and_generator_match_delta_operator(n, j):
+    """orc_matvec_rows / orc_generator are the checkers of the multi-pass regime (n up to 2^20,
+    where even the matrix-free full product is too slow): pinned to the literal delta_h^beta
+    operator through eq3.3, and the rows to the full product bitwise."""
+    p = O.Problem(alpha=0.6, beta=1.7, n=n, M=6, gamma=(O.COS, 0.9), dplus=(O.ONE_PLUS_T, 0.8),
+                  dminus=(O.ONE_PLUS_T2, 1.4), src=O.SRC_MMS3)
+    D = _delta_matrix(p, j)
+    eta, sigma = O.eta(p.alpha, p.tau, j), p.sigma
+    x = np.random.default_rng(11 * n + j).standard_normal(n)
+    rows = np.array([0, 1, n // 2, n - 2, n - 1])
+    for which, Mx in ((0, eta * np.eye(n) - sigma * D), (1, eta * np.eye(n) + (1 - sigma) * D)):
+        y = O.matvec_rows(p, j, which, x, rows)
+        np.testing.assert_array_equal(y, O.matvec(p, j, which, x)[rows])
+        assert np.abs(y - (Mx @ x)[rows]).max() <= 1e-13 * np.abs(Mx).sum(1).max() * np.abs(x).max()
+        col, row = O.generator(p, j, which)
+        np.testing.assert_allclose(col, Mx[:, 0], rtol=1e-14, atol=1e-14 * np.abs(Mx).max())
+        np.testing.assert_allclose(row, Mx[0, :], rtol=1e-14, atol=1e-14 * np.abs(Mx).max())
+        if which == 0:
+            U = O.solve(p)
+            np.testing.assert_array_equal(O.rhs_rows(p, j, U[: j + 1], rows),
+                                          O.rhs_nodense(p, j, U[: j + 1])[rows])
+        # Toeplitz: every diagonal of the literal operator is constant
+        for k in range(-n + 1, n):
+            dg = np.diagonal(Mx, k)
+            np.testing.assert_allclose(dg, dg[0], rtol=1e-13, atol=1e-13 * np.abs(Mx).max())
+
+
 def test_openmp_rows_are_bitwise_thread_independent():
     """oracle.c splits independent rows across OpenMP threads; the results must not depend on
     the thread count (every row's summation order is fixed)."""

@@ -232,7 +232,7 @@ def lib_hash() -> str:
 
 def traffic_key(args) -> str:
     return f"{args.config}/{args.method}/{args.precond}" + ("/warm" if args.warm else "") + \
-        ("/tres" if args.true_res else "")
+        ("/tres" if args.true_res else "") + ("/pipe" if getattr(args, "pipelined", False) else "")
 
 
 def base_config(args):
@@ -285,6 +285,8 @@ def main():
                     help="also compute the per-level true residual (an extra A application per level; "
                          "off by default: the paper's stopping rule uses the recurrence residual, P:922-924)")
     ap.add_argument("--warm", action="store_true", help="NEXT-3 warm start x0 = u^j")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="NEXT-3 two-reduction BiCGSTAB (merged dot products)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -326,7 +328,7 @@ def main():
     insts, scaling, units_total = build_instances(args.config, world, rank)
     n, M = insts[0].n, insts[0].M
     solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster,
-                     true_residual=args.true_res, x0_warm=args.warm)
+                     true_residual=args.true_res, x0_warm=args.warm, pipelined=args.pipelined)
     stream = torch.cuda.Stream(dev)
     t_init0 = time.perf_counter()
     s = tsf.Solver(insts, stream=stream, **solver_kw)
@@ -445,6 +447,7 @@ def main():
             "config": {**base_config(args), "instances": units_total, "cluster": info.cluster,
                        "exchange": ["local", "staged DSMEM push", "chunked via L2", "multi-pass via L2"][info.exchange],
                        "true_residual": bool(args.true_res), "x0_warm": bool(args.warm),
+                       "pipelined": bool(args.pipelined),
                        "l2": "flushed between steps (512 MiB write)",
                        "timed": "k_solve + level counter" + (" + NCCL all-gather of u^M and stats" if do_gather else "")},
             "krylov_iters_per_s": iters_per_s,

@@ -114,7 +114,13 @@ typedef struct {
  * ||r_k|| < tol ||r_0|| = tol ||g||; 1 = initial guess u^j (one extra A application per level,
  * r_0 = g - A u^j) with the same g-relative stop ||r_k|| < tol ||g||.  Not for TSF_GSF.
  * true_residual: 1 = at every level exit also compute ||g - A u^{j+1}|| / ||g|| with a fresh
- * operator application (tsf_get_true_residuals; SURVEY reading c13), 0 = skip it. */
+ * operator application (tsf_get_true_residuals; SURVEY reading c13), 0 = skip it.
+ * pipelined (NEXT-3, BiCGSTAB and the GSF path's setup/level-0 solves only): 1 = two cluster
+ * reductions per iteration instead of four -- r^.v, r.v, v.v, r.r in one, t.s, t.t, r^.s, r^.t
+ * in the other; ||s||^2 = ||r||^2 - 2 alpha r.v + alpha^2 v.v, ||r'||^2 = ||s||^2 - 2 omega t.s +
+ * omega^2 t.t and rho' = r^.s - omega r^.t by expansion (exact reduction as a fallback when the
+ * expansion cancels), and the x, r and p updates in one vector pass.  Same iterates as 0 in
+ * exact arithmetic; the stopping test reads the expanded norms. */
 typedef struct {
   int32_t method;     /* tsf_method  */
   int32_t precond;    /* tsf_precond */
@@ -123,6 +129,7 @@ typedef struct {
   int32_t cluster;
   int32_t x0_warm;
   int32_t true_residual;
+  int32_t pipelined;
 } tsf_solver;
 
 /* Plan summary (host only, no GPU needed). */

@@ -1864,7 +1864,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
       // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
       // and geometry are selected per h) so the hot loop's code stays small for the instruction
       // cache; the vector work before/after each application is dispatched on h.
-      double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0;
+      double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0, ss_est = 0.0;
       for (int h = 0;; h = (h + 1) & 3) {
         const bool isP = !(h & 1);
         if (isP && !prec) {
@@ -1883,6 +1883,109 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
             Dst[e] = z;
             AX[e] = z;
             AX[e + npc] = zero2();
+          }
+          continue;
+        }
+        if (h == 1 && P.pipelined) {
+          // NEXT-3 (two reductions per iteration): r^.v, r.v, v.v, r.r in one cluster sum;
+          // ||s||^2 = ||r||^2 - 2 alpha r.v + alpha^2 v.v (exact reduction if it cancels)
+          double d[4] = {0.0, 0.0, 0.0, 0.0};
+          TSF_FOR_E(npc) {
+            const double2 v = Y[e], rv = R[e];
+            VV[e] = v;
+            d[0] += cdot(RH[e], v);
+            d[1] += cdot(rv, v);
+            d[2] += cdot(v, v);
+            d[3] += cdot(rv, rv);
+          }
+          csum<C, 4>(d, sm, xs);
+          if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+          alpha = rho / d[0];
+          ss_est = d[3] - 2.0 * alpha * d[1] + alpha * alpha * d[2];
+          const bool exact = !(ss_est > 1e-10 * d[3]);
+          double ss[1] = {0.0};
+          if (!exact && sqrt(ss_est) < P.tol * rn0) {
+            TSF_FOR_E(npc) { X[e] = caxpy(alpha, PH[e], X[e]); }
+            hs += 1;
+            relres = sqrt(ss_est) / rn0;
+            break;
+          }
+          TSF_FOR_E(npc) {
+            const double2 sv = caxpy(-alpha, VV[e], R[e]);
+            S[e] = sv;
+            AX[e] = sv;
+            if (exact) ss[0] += cdot(sv, sv);
+          }
+          if (exact) {
+            csum<C, 1>(ss, sm, xs);
+            ss_est = ss[0];
+            if (sqrt(ss[0]) < P.tol * rn0) {
+              TSF_FOR_E(npc) { X[e] = caxpy(alpha, PH[e], X[e]); }
+              hs += 1;
+              relres = sqrt(ss[0]) / rn0;
+              break;
+            }
+          }
+          continue;
+        }
+        if (h == 3 && P.pipelined) {
+          // t.s, t.t, r^.s, r^.t in one cluster sum; omega; ||r'||^2 and rho' = r^.r' by
+          // expansion; then x, r and the next p in one pass
+          double tt[4] = {0.0, 0.0, 0.0, 0.0};
+          TSF_FOR_E(npc) {
+            const double2 t = Y[e], sv = S[e], rh = RH[e];
+            tt[0] += cdot(t, sv);
+            tt[1] += cdot(t, t);
+            tt[2] += cdot(rh, sv);
+            tt[3] += cdot(rh, t);
+          }
+          csum<C, 4>(tt, sm, xs);
+          if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+          omega = tt[0] / tt[1];
+          double rn2 = ss_est - 2.0 * omega * tt[0] + omega * omega * tt[1];
+          const double rho_n = tt[2] - omega * tt[3];
+          hs += 2;
+          bool exact = !(rn2 > 1e-10 * ss_est);
+          bool done = false;
+          if (!exact) {
+            relres = sqrt(rn2) / rn0;
+            if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+            done = relres < P.tol || hs >= 2 * P.maxit || !(fabs(rho_n) > 1e-300);
+          }
+          if (!exact && !done) {
+            beta = (rho_n / rho) * (alpha / omega);
+            rho = rho_n;
+            TSF_FOR_E(npc) {
+              X[e] = caxpy(omega, SH[e], caxpy(alpha, PH[e], X[e]));
+              const double2 rn = caxpy(-omega, Y[e], S[e]);
+              R[e] = rn;
+              const double2 pv = caxpy(beta, caxpy(-omega, VV[e], PV[e]), rn);
+              PV[e] = pv;
+              AX[e] = pv;
+            }
+            continue;
+          }
+          // convergence, a limit, or a cancelled expansion: the plain update with exact norms
+          double rr[2] = {0.0, 0.0};
+          TSF_FOR_E(npc) {
+            X[e] = caxpy(omega, SH[e], caxpy(alpha, PH[e], X[e]));
+            const double2 rn = caxpy(-omega, Y[e], S[e]);
+            R[e] = rn;
+            rr[0] += cdot(RH[e], rn);
+            rr[1] += cdot(rn, rn);
+          }
+          csum<C, 2>(rr, sm, xs);
+          relres = sqrt(rr[1]) / rn0;
+          if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; break; }
+          if (relres < P.tol) break;
+          if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; break; }
+          if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; break; }
+          beta = (rr[0] / rho) * (alpha / omega);
+          rho = rr[0];
+          TSF_FOR_E(npc) {
+            const double2 pv = caxpy(beta, caxpy(-omega, VV[e], PV[e]), R[e]);
+            PV[e] = pv;
+            AX[e] = pv;
           }
           continue;
         }

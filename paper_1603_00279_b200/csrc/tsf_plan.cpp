@@ -148,6 +148,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.ftab_dev = (p[0].src_kind == TSF_SRC_TABLE && p[0].f_table_on_device) ? 1 : 0;
   P.x0_warm = s->x0_warm ? 1 : 0;
   P.true_res = s->true_residual ? 1 : 0;
+  P.pipelined = s->pipelined ? 1 : 0;
   const int64_t n = P.n;
   int C = s->cluster;
   if (C == 0) {
@@ -373,7 +374,8 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.fptr = reinterpret_cast<const double *const *>(ws + pl.off_fptr);
   d.ftab_dev = pl.ftab_dev;
   d.x0_warm = pl.x0_warm;
-  d.true_res = pl.true_res; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
+  d.true_res = pl.true_res;
+  d.pipelined = pl.pipelined; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
   return d;
 }
 

@@ -406,6 +406,46 @@ def test_warm_start_parity_and_fewer_iterations(method, cluster):
     assert its[1] < its[0], its
 
 
+@pytest.mark.parametrize("cluster,precond,n", [(1, "strang", 1024), (4, "tchan", 1024), (8, "strang", 2048),
+                                              (16, "strang", 4096)])
+def test_pipelined_bicgstab_parity_and_iterations(cluster, precond, n):
+    """NEXT-3 two-reduction BiCGSTAB (dot products merged, norms by expansion): the same
+    iterates as the four-reduction loop in exact arithmetic, so the oracle parity bar holds and
+    the iteration counts agree within one iteration per level; the reported relres is exact."""
+    inst, p = pair(0.8, 1.8, n, 12, gamma=(O.COS, 1.0), dplus=(O.ONE_PLUS_T, 1.0),
+                   dminus=(O.ONE_PLUS_T2, 1.0))
+    Uo = O.solve(p)
+    its = []
+    for pipe in (False, True):
+        s = tsf.Solver([inst], precond=precond, cluster=cluster, pipelined=pipe)
+        U = run_levels(s, 12)[0]
+        assert max_rel(U, Uo) <= RTOL, pipe
+        it, rr, st = s.stats()
+        assert (st == 0).all() and rr.max() < 1e-12
+        tr = s.true_residuals()
+        assert tr.max() < 1e-10
+        its.append(it[0])
+    # rounding alone moves a level's exit by at most one full iteration either way
+    assert np.abs(its[0] - its[1]).max() <= 2, its
+    assert abs(int(its[0].sum()) - int(its[1].sum())) <= 0.06 * its[0].sum(), its
+
+
+def test_pipelined_bicgstab_batched_unstaged_path(monkeypatch):
+    """The two-reduction loop on the chunked (C5) kernel path with HBM vectors, batched."""
+    monkeypatch.setenv("TSF_STAGED", "0")
+    monkeypatch.setenv("TSF_VSMEM", "0")
+    monkeypatch.setenv("TSF_CHUNK", "2")
+    pairs = [pair(0.3 + 0.2 * b, 1.4 + 0.2 * b, 4096, 6, gamma=(O.CONST, 0.3 * b),
+                  dplus=(O.ONE_PLUS_T, 0.8 + 0.3 * b), dminus=(O.ONE_PLUS_T, 1.5 - 0.2 * b)) for b in range(3)]
+    s = tsf.Solver([a for a, _ in pairs], cluster=16, pipelined=True)
+    assert s.info.exchange == 2
+    U = run_levels(s, 6)
+    for b, (_, p) in enumerate(pairs):
+        assert max_rel(U[b], O.solve(p)) <= RTOL, b
+    it, rr, st = s.stats()
+    assert (st == 0).all() and rr.max() < 1e-12
+
+
 @pytest.mark.parametrize("method", ["bicgstab", "cgnr", "pcgs", "gsf"])
 def test_true_residual_is_reported_at_every_level(method):
     """SURVEY reading c13: the stopping rule uses the recurrence residual; the true residual

@@ -96,14 +96,30 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(n, M, iters_half_rows, method, src_units):
-    """SURVEY 8(d) model per instance: 8n (j + 3 + src + 8) compulsory/RHS bytes per level
-    plus 8n * units * I_j for the streamed Krylov iterations (I_j = iterations of level j)."""
+def hist_units(j, M, hblock=0):
+    """History rows (n-vectors) level j must move: j rows read by the direct sum (eq3.1); with
+    the NEXT-3 blocked sum (block b, J0 = j - j mod b) the rows since J0 plus one partial-sum row,
+    and at a block start the pass over d^0..d^{J0-1} plus the b partial sums it writes."""
+    if hblock <= 0 or j == 0:
+        return j
+    J0 = j - j % hblock
+    if J0 == 0:
+        return j
+    u = (j - J0) + 1
+    if j == J0:
+        u += J0 + min(hblock, M - J0)
+    return u
+
+
+def algorithmic_bytes(n, M, iters_half_rows, method, src_units, hblock=0):
+    """SURVEY 8(d) model per instance: 8n (h_j + 3 + src + 8) compulsory/RHS bytes per level
+    (h_j = history rows, j for the direct sum) plus 8n * units * I_j for the streamed Krylov
+    iterations (I_j = iterations of level j)."""
     units = KRYLOV_UNITS[method]
     total = 0.0
     for row in iters_half_rows:
         for j in range(M):
-            total += 8.0 * n * (j + 3 + src_units + 8) + 8.0 * n * units * (row[j] / 2.0)
+            total += 8.0 * n * (hist_units(j, M, hblock) + 3 + src_units + 8) + 8.0 * n * units * (row[j] / 2.0)
             if method == "gsf" and j >= 1:
                 total += 8.0 * n * GSF_UNITS_PER_LEVEL
     return total
@@ -232,7 +248,8 @@ def lib_hash() -> str:
 
 def traffic_key(args) -> str:
     return f"{args.config}/{args.method}/{args.precond}" + ("/warm" if args.warm else "") + \
-        ("/tres" if args.true_res else "") + ("/pipe" if getattr(args, "pipelined", False) else "")
+        ("/tres" if args.true_res else "") + ("/pipe" if getattr(args, "pipelined", False) else "") + \
+        (f"/hb{args.hist_block}" if getattr(args, "hist_block", 0) else "")
 
 
 def base_config(args):
@@ -285,6 +302,8 @@ def main():
                     help="also compute the per-level true residual (an extra A application per level; "
                          "off by default: the paper's stopping rule uses the recurrence residual, P:922-924)")
     ap.add_argument("--warm", action="store_true", help="NEXT-3 warm start x0 = u^j")
+    ap.add_argument("--hist-block", type=int, default=0,
+                    help="NEXT-3 blocked history sum with this block length (0 = direct)")
     ap.add_argument("--pipelined", action="store_true",
                     help="NEXT-3 two-reduction BiCGSTAB (merged dot products)")
     args = ap.parse_args()
@@ -328,7 +347,8 @@ def main():
     insts, scaling, units_total = build_instances(args.config, world, rank)
     n, M = insts[0].n, insts[0].M
     solver_kw = dict(method=args.method, precond=args.precond, cluster=args.cluster,
-                     true_residual=args.true_res, x0_warm=args.warm, pipelined=args.pipelined)
+                     true_residual=args.true_res, x0_warm=args.warm, pipelined=args.pipelined,
+                     hist_block=args.hist_block)
     stream = torch.cuda.Stream(dev)
     t_init0 = time.perf_counter()
     s = tsf.Solver(insts, stream=stream, **solver_kw)
@@ -390,7 +410,7 @@ def main():
     value = levels_job * args.steps / total_s
     iters_per_s = iters_job * args.steps / total_s
     src_units = 1 if insts[0].source == "table" else (4 if insts[0].source in ("mms3", "exa") else 0)
-    abytes = algorithmic_bytes(n, M, it_half, args.method, src_units)   # per launch, this rank
+    abytes = algorithmic_bytes(n, M, it_half, args.method, src_units, args.hist_block)   # per launch, this rank
     kernel_s = statistics.mean(kms) / 1000.0       # the k_solve launch, CUDA events on its stream
     achieved = abytes / kernel_s / 1e9
     peak, peak_kind = peaks()
@@ -447,7 +467,7 @@ def main():
             "config": {**base_config(args), "instances": units_total, "cluster": info.cluster,
                        "exchange": ["local", "staged DSMEM push", "chunked via L2", "multi-pass via L2"][info.exchange],
                        "true_residual": bool(args.true_res), "x0_warm": bool(args.warm),
-                       "pipelined": bool(args.pipelined),
+                       "pipelined": bool(args.pipelined), "hist_block": args.hist_block,
                        "l2": "flushed between steps (512 MiB write)",
                        "timed": "k_solve + level counter" + (" + NCCL all-gather of u^M and stats" if do_gather else "")},
             "krylov_iters_per_s": iters_per_s,

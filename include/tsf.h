@@ -120,7 +120,13 @@ typedef struct {
  * in the other; ||s||^2 = ||r||^2 - 2 alpha r.v + alpha^2 v.v, ||r'||^2 = ||s||^2 - 2 omega t.s +
  * omega^2 t.t and rho' = r^.s - omega r^.t by expansion (exact reduction as a fallback when the
  * expansion cancels), and the x, r and p updates in one vector pass.  Same iterates as 0 in
- * exact arithmetic; the stopping test reads the expanded norms. */
+ * exact arithmetic; the stopping test reads the expanded norms.
+ * hist_block (NEXT-3, blocked time convolution of the memory term of eq3.1): 0 = every level
+ * sums its whole history (j rows, O(M^2) row reads per run); b in {2,4,...,64} = at each block
+ * start J0 = kb one pass over the rows d^0..d^{J0-1} forms the partial sums of all b levels of
+ * the block (kappa e_j d^0 + sum_{s=1}^{J0-1} kappa chat_{j-s} d^s, j = J0..J0+b-1), and level j
+ * adds only its < b rows since J0: ~(J0/b + j - J0 + 2) row reads per level instead of j.  Same
+ * terms, grouped differently (rounding only).  Disables the history-helper clusters. */
 typedef struct {
   int32_t method;     /* tsf_method  */
   int32_t precond;    /* tsf_precond */
@@ -130,6 +136,7 @@ typedef struct {
   int32_t x0_warm;
   int32_t true_residual;
   int32_t pipelined;
+  int32_t hist_block;
 } tsf_solver;
 
 /* Plan summary (host only, no GPU needed). */

@@ -41,7 +41,8 @@ class TsfProblem(C.Structure):
 class TsfSolver(C.Structure):
     _fields_ = [("method", C.c_int32), ("precond", C.c_int32), ("tol", C.c_double),
                 ("maxit", C.c_int32), ("cluster", C.c_int32), ("x0_warm", C.c_int32),
-                ("true_residual", C.c_int32), ("pipelined", C.c_int32)]
+                ("true_residual", C.c_int32), ("pipelined", C.c_int32),
+                ("hist_block", C.c_int32)]
 
 
 class TsfPlanInfo(C.Structure):

@@ -69,6 +69,7 @@ struct Inst {
   double2 *gsf;          // NEXT-2: spectra of the 4 triangular GSF factors [4][n+1] (task order)
   double2 *xg;           // unstaged clusters: L2 exchange buffer [C][L1e] of the local FFT outputs
   double2 *xa;           // multi-pass regime: apply input/output buffer [C][L1e] (natural local order)
+  double *hb;            // blocked history: partial sums of the current block's levels [hblock][n]
   const double *phi;     // u^0 (permuted chunks)
   const double *fdev;    // borrowed device source table (natural order) or nullptr
   int32_t *it, *st;
@@ -94,6 +95,7 @@ __device__ __forceinline__ Inst inst_view(const DevParams &P, int b) {
   I.gsf = reinterpret_cast<double2 *>(base + P.o_gsf);
   I.xg = reinterpret_cast<double2 *>(base + P.o_xg);
   I.xa = reinterpret_cast<double2 *>(base + P.o_xa);
+  I.hb = reinterpret_cast<double *>(base + P.o_hb);
   I.it = reinterpret_cast<int32_t *>(base + P.o_it);
   I.rr = reinterpret_cast<double *>(base + P.o_rr);
   I.trr = reinterpret_cast<double *>(base + P.o_trr);
@@ -1504,11 +1506,81 @@ struct T3 { double2 a, b, c; };
 struct T5 { double2 a, b, c, d, f; };
 
 // ------------------------------------------------------------------------ RHS (alg1 step 2)
+// NEXT-3 blocked history sum (tsf.h hist_block).  Levels J0 = kb .. J0+b-1 form a block.  At the
+// block start one pass over the rows d^0..d^{J0-1} (each row read once, HU rows in flight per
+// thread) forms for every level of the block
+//   HB[q] = kappa e_{J0+q} d^0 + sum_{s=1}^{J0-1} kappa chat_{J0+q-s} d^s        (q < b),
+// and level j adds its rows since the block start: Hs = HB[j-J0] + sum_{s=max(1,J0)}^{j-1}
+// kappa chat_{j-s} d^s (+ kappa e_j d^0 in block 0, where HB is not used).  Element e is only
+// ever touched by thread e mod kThreads (same thread writes HB and reads it later).
+template <int QB>
+__device__ __forceinline__ void hist_block_pass(const Inst &I, int64_t J0, int64_t M, uint32_t r, int npc,
+                                                const double2 *__restrict__ H, double2 *__restrict__ HB,
+                                                int64_t hstride) {
+  constexpr int HU = 4;
+  for (int e = threadIdx.x; e < npc; e += kThreads) {
+    double2 acc[QB];
+    const double2 d0 = H[e];
+#pragma unroll
+    for (int q = 0; q < QB; ++q) acc[q] = (J0 + q < M) ? cscale(d0, I.hwe[J0 + q]) : zero2();
+    int64_t s = 1;
+    for (; s + HU - 1 <= J0 - 1; s += HU) {
+      double2 v[HU];
+#pragma unroll
+      for (int u = 0; u < HU; ++u) v[u] = H[(s + u) * hstride + e];
+#pragma unroll
+      for (int u = 0; u < HU; ++u)
+#pragma unroll
+        for (int q = 0; q < QB; ++q) acc[q] = caxpy(I.hwc[min(J0 + q - s - u, M - 1)], v[u], acc[q]);
+    }
+    for (; s <= J0 - 1; ++s) {
+      const double2 v = H[s * hstride + e];
+#pragma unroll
+      for (int q = 0; q < QB; ++q) acc[q] = caxpy(I.hwc[min(J0 + q - s, M - 1)], v, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < QB; ++q) HB[q * hstride + e] = acc[q];
+  }
+}
+
+__device__ __forceinline__ void hist_blocked(const DevParams &P, const Inst &I, int64_t j, uint32_t r,
+                                             const double2 *__restrict__ H, double2 *__restrict__ Hs, int b) {
+  const int npc = P.L1p;
+  const int64_t hstride = P.n / 2;
+  const int64_t J0 = j - j % b;
+  double2 *HB = reinterpret_cast<double2 *>(I.hb) + r * npc;
+  if (j == J0 && J0 > 0) {
+    // the block's partial sums, in sub-blocks of at most 16 levels (register budget)
+    for (int q0 = 0; q0 < b; q0 += 16) {
+      const int qb = b - q0 < 16 ? b - q0 : 16;
+      double2 *dst = HB + q0 * hstride;
+      if (qb == 16) hist_block_pass<16>(I, J0 + q0, P.M, r, npc, H, dst, hstride);
+      else if (qb == 8) hist_block_pass<8>(I, J0 + q0, P.M, r, npc, H, dst, hstride);
+      else if (qb == 4) hist_block_pass<4>(I, J0 + q0, P.M, r, npc, H, dst, hstride);
+      else hist_block_pass<2>(I, J0 + q0, P.M, r, npc, H, dst, hstride);
+    }
+  }
+  const int64_t s0 = J0 > 1 ? J0 : 1;
+  const double2 *Bj = HB + (j - J0) * hstride;
+  for (int e = threadIdx.x; e < npc; e += kThreads) {
+    double2 a = J0 > 0 ? Bj[e] : cscale(H[e], I.hwe[j]);
+    double2 c = zero2();
+    int64_t s = s0;
+    for (; s + 1 <= j - 1; s += 2) {
+      const double2 v0 = H[s * hstride + e], v1 = H[(s + 1) * hstride + e];
+      a = caxpy(I.hwc[j - s], v0, a);
+      c = caxpy(I.hwc[j - s - 1], v1, c);
+    }
+    if (s <= j - 1) a = caxpy(I.hwc[j - s], H[s * hstride + e], a);
+    Hs[e] = cadd(a, c);
+  }
+}
+
 // g = B u^j - [kappa e_j d^0 + sum_{s=1}^{j-1} kappa chat_{j-s} d^s] + f^{j+sigma}
 // First half: the memory term into Hsum and u^j (zero-padded) into A; the caller applies B.
 template <int C, bool BIG>
 __device__ __forceinline__ void rhs_pre(const DevParams &P, const Smem &sm, const Inst &I, int64_t j, uint32_t r,
-                                        const double2 *U, double2 *Hsum, bool use_pre) {
+                                        const double2 *U, double2 *Hsum, bool use_pre, int hblock = 0) {
   // (use_pre is dropped below when the helpers do not deliver in time)
   const int npc = P.L1p;
   const int64_t n = P.n;
@@ -1543,6 +1615,8 @@ __device__ __forceinline__ void rhs_pre(const DevParams &P, const Smem &sm, cons
     const double2 *Pj = reinterpret_cast<const double2 *>(P.pre) + (j & 1) * hstride + r * npc;
     const double w1 = I.hwc[1];
     TSF_FOR_E(npc) { Hs[e] = caxpy(w1, H[(j - 1) * hstride + e], __ldcg(Pj + e)); }
+  } else if (j >= 1 && hblock > 0) {
+    hist_blocked(P, I, j, r, H, Hs, hblock);
   } else if (j >= 1) {
     // the same summation order as the helpers (P^j over rows 1..j-2 with HU-row batches and two
     // accumulators, then + chat_1 d^{j-1}), so step-wise and helper-assisted runs agree bitwise;
@@ -1765,7 +1839,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
   double g2[1] = {0.0};
   int ph;
   if (mode == 0) {
-    rhs_pre<C, BIG>(P, sm, I, j, r, V.U, V.X, P.helpers > 0 && j >= 2 && j >= j0 + 1);
+    rhs_pre<C, BIG>(P, sm, I, j, r, V.U, V.X, P.helpers > 0 && j >= 2 && j >= j0 + 1, P.hblock);
     ph = S_RHS;
   } else {
     // e_1: packed z_0 = (1, 0) on CTA 0; e_n: z_{n/2-1} = (0, 1) on CTA (n/2-1) mod C
@@ -2480,7 +2554,8 @@ cudaError_t launch_solve_k(K kern, const Plan &pl, const DevParams &dp0, int32_t
   DevParams dp = dp0;
   dp.helpers = 0;
   int grid = pl.B * pl.C;
-  if (pl.B == 1 && pl.C > 1 && nlev >= 3 && mode == 0 && std::getenv("TSF_NO_HELPERS") == nullptr) {
+  if (pl.B == 1 && pl.C > 1 && nlev >= 3 && mode == 0 && pl.hblock == 0 &&
+      std::getenv("TSF_NO_HELPERS") == nullptr) {
     const int64_t cta_need = (pl.n / 2 + kThreads - 1) / kThreads;
     int hcl = int((cta_need + pl.C - 1) / pl.C);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));

@@ -113,6 +113,8 @@ int validate(const tsf_problem *p, int32_t B, const tsf_solver *s) {
   if (s->precond != TSF_STRANG && s->precond != TSF_TCHAN && s->precond != TSF_NOPREC)
     return fail("unknown preconditioner %g", s->precond);
   if (!(s->tol > 0.0)) return fail("tol=%g must be > 0", s->tol);
+  if (s->hist_block != 0 && (!is_pow2(s->hist_block) || s->hist_block < 2 || s->hist_block > 64))
+    return fail("hist_block=%g must be 0 or a power of two in [2, 64]", s->hist_block);
   if (s->maxit < 1) return fail("maxit=%g must be >= 1", s->maxit);
   return TSF_OK;
 }
@@ -149,6 +151,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.x0_warm = s->x0_warm ? 1 : 0;
   P.true_res = s->true_residual ? 1 : 0;
   P.pipelined = s->pipelined ? 1 : 0;
+  P.hblock = s->hist_block;
   const int64_t n = P.n;
   int C = s->cluster;
   if (C == 0) {
@@ -249,6 +252,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.o_gsf = q;   q = up(q + (s->method == TSF_GSF ? size_t(4) * size_t(n + 1) * 16 : 0));
   P.o_xg = q;    q = up(q + (C > 1 && !P.staged ? size_t(n) * 16 : 0));   // L2 exchange (unstaged)
   P.o_xa = q;    q = up(q + (P.big ? size_t(n) * 16 : 0));                 // apply buffer (multi-pass)
+  P.o_hb = q;    q = up(q + size_t(P.hblock) * size_t(n) * 8);             // blocked history sums
   P.stride = q;
   P.total = P.off_inst + P.stride * size_t(B);
   *pl = P;
@@ -375,7 +379,8 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.ftab_dev = pl.ftab_dev;
   d.x0_warm = pl.x0_warm;
   d.true_res = pl.true_res;
-  d.pipelined = pl.pipelined; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
+  d.pipelined = pl.pipelined;
+  d.hblock = pl.hblock; d.o_hb = pl.o_hb; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
   return d;
 }
 

@@ -67,6 +67,8 @@ struct DevParams {
   int32_t x0_warm;                 // NEXT-3: Krylov initial guess u^j (else 0)
   int32_t true_res;                // compute ||g - A u^{j+1}|| / ||g|| at every level exit
   int32_t pipelined;               // NEXT-3: BiCGSTAB with two cluster reductions per iteration
+  int32_t hblock;                  // NEXT-3: blocked history sum, block length (0 = direct)
+  int64_t o_hb;                    // blocked history: partial sums of the block's levels [hblock][n]
 };
 
 struct Plan {
@@ -87,7 +89,8 @@ struct Plan {
   size_t off_tw = 0, off_slot_e = 0, off_slot_p = 0, off_sq_e = 0, off_sq_p = 0;
   size_t off_level = 0, off_prof = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
   size_t off_sync = 0, off_pre = 0, off_fptr = 0;
-  int32_t x0_warm = 0, true_res = 0, pipelined = 0;
+  int32_t x0_warm = 0, true_res = 0, pipelined = 0, hblock = 0;
+  int64_t o_hb = 0;
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
   int64_t o_par, o_omega, o_lwe, o_lwp, o_lev, o_hwc, o_hwe, o_scal, o_basis, o_ftab;

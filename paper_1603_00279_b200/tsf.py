@@ -86,7 +86,7 @@ def marshal(instances: Sequence[Instance]):
 
 
 def make_solver_struct(method="bicgstab", precond="strang", tol=1e-12, maxit=None, cluster=0,
-                       x0_warm=False, true_residual=True, pipelined=False):
+                       x0_warm=False, true_residual=True, pipelined=False, hist_block=0):
     s = L.TsfSolver()
     s.method = METHODS[method]
     s.precond = PRECONDS[precond]
@@ -96,6 +96,7 @@ def make_solver_struct(method="bicgstab", precond="strang", tol=1e-12, maxit=Non
     s.x0_warm = int(bool(x0_warm))
     s.true_residual = int(bool(true_residual))
     s.pipelined = int(bool(pipelined))
+    s.hist_block = int(hist_block)
     return s
 
 
@@ -113,7 +114,7 @@ class Solver:
 
     def __init__(self, instances: Sequence[Instance], method="bicgstab", precond="strang",
                  tol=1e-12, maxit=None, cluster=0, device=None, stream=None, workspace=None,
-                 x0_warm=False, true_residual=True, pipelined=False):
+                 x0_warm=False, true_residual=True, pipelined=False, hist_block=0):
         import torch
         self.lib = L.load()
         self.instances = list(instances)
@@ -123,7 +124,7 @@ class Solver:
         self.h2d_bytes = sum(a.nbytes for arrs in keep for a in arrs.values() if isinstance(a, np.ndarray))
         self._borrowed = [arrs["f_dev"] for arrs in keep if "f_dev" in arrs]
         self._solver = make_solver_struct(method, precond, tol, maxit, cluster, x0_warm, true_residual,
-                                          pipelined)
+                                          pipelined, hist_block)
         info = L.TsfPlanInfo()
         L.check(self.lib.tsf_plan(probs, self.B, C.byref(self._solver), C.byref(info)), "tsf_plan")
         self.info = info

@@ -124,6 +124,26 @@ def test_planner_multi_pass_regime(lg):
                            dminus=const(0.5))]) if (kmax := 1 << 20) else None
 
 
+def test_hist_block_option_validated_and_row_model():
+    """hist_block: 0 or a power of two in [2, 64]; the bench's history row model: the direct sum
+    reads j rows at level j, the blocked sum about J0/b + (j - J0) + 2 per level."""
+    import bench
+    inst = CONFIGS["C1"]()[0]
+    for bad in (3, 1, 128, -2):
+        with pytest.raises(L.TsfError, match="hist_block"):
+            tsf.plan([inst], hist_block=bad)
+    base = tsf.plan([inst]).workspace_bytes
+    assert tsf.plan([inst], hist_block=16).workspace_bytes >= base + 16 * inst.n * 8
+    M = 256
+    direct = sum(bench.hist_units(j, M) for j in range(M))
+    blocked = sum(bench.hist_units(j, M, 16) for j in range(M))
+    assert direct == M * (M - 1) // 2
+    # block starts read J0 rows and write 16 partial sums; other levels <= 16 rows
+    assert blocked == sum(j for j in range(16)) + sum(
+        (j % 16) + 1 + (j + 16 if j % 16 == 0 else 0) for j in range(16, M))
+    assert blocked < direct / 4
+
+
 def test_init_rejects_small_workspace_without_touching_the_gpu():
     lib = L.load()
     probs, keep = tsf.marshal(CONFIGS["C1"]())

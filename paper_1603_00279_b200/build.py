@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import shutil
 import subprocess
 import sys
 
@@ -31,10 +32,11 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, verbose: bool, profile: bool = False, extra=(), variant: str = "") -> str:
+def _compile(src: str, verbose: bool, profile: bool = False, extra=(), variant: str = "",
+             src_dir: str = CSRC) -> str:
     tag = ("_prof" if profile else "") + (f"_{variant}" if variant else "")
     obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + tag + ".o")
-    cmd = [NVCC, *FLAGS, *(["-DTSF_PROFILE"] if profile else []), *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *FLAGS, *(["-DTSF_PROFILE"] if profile else []), *extra, "-c", os.path.join(src_dir, src), "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
@@ -52,8 +54,16 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, var
         return lib
     os.makedirs(LIBDIR, exist_ok=True)
     extra = [f"-D{d}" for d in defines]
-    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose, profile, extra, variant), SOURCES))
+    # compile from a snapshot of the sources so edits during a long build cannot mix versions
+    # (kept under lib/, which travels to the GPU box, so ncu --import-source finds the lines)
+    snap = os.path.join(LIBDIR, "snap_" + (os.path.basename(lib).replace(".so", "")))
+    shutil.rmtree(snap, ignore_errors=True)
+    if True:
+        src_dir = os.path.join(snap, "pkg", "csrc")     # csrc/../../include resolves inside snap
+        shutil.copytree(CSRC, src_dir)
+        shutil.copytree(os.path.join(HERE, "..", "include"), os.path.join(snap, "include"))
+        with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            objs = list(ex.map(lambda s: _compile(s, verbose, profile, extra, variant, src_dir), SOURCES))
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs])
     os.replace(lib + ".tmp", lib)
     return lib

@@ -217,6 +217,7 @@ struct Smem {
   double *wred, *cred;
   double *red;                       // push reductions: [2][16][4] CTA partials (double-buffered)
   uint64_t *mbar;                    // mbarriers: [0] exchange-in B, [1] exchange-back O, [2..3] red
+  double2 *twc;                      // W_C^e, e < C (column-DFT twiddles of the staged column stage)
   int *flag;                         // CTA-wide broadcast word.  NOTE: the solve kernels declare NO
                                      // static __shared__ variable: one would shift the dynamic buffers
                                      // off their 128-byte alignment and break the bank-conflict-free
@@ -279,6 +280,7 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
   s.red = d + 48;
   s.mbar = reinterpret_cast<uint64_t *>(d + 48 + 128);
   s.flag = reinterpret_cast<int *>(d + 48 + 128 + 4);
+  s.twc = reinterpret_cast<double2 *>(d + 48 + 128 + 4 + 2);
   return s;
 }
 
@@ -288,6 +290,7 @@ __device__ __forceinline__ double2 twid(const Smem &sm, int e) {
 }
 
 __device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col);
+__device__ __forceinline__ int dperm(int p, int l);
 
 // Kernel prologue: local-FFT twiddles and (resident mode) this CTA's constant tables, copied
 // from the accurate global tables (twiddles tw[x] = exp(-2 pi i x / twN)).
@@ -302,29 +305,22 @@ __device__ __forceinline__ void load_constants(const DevParams &P, const double2
     for (int i = threadIdx.x; i < tw_lo_len(L1e); i += kThreads) sm.tlo[i] = tw[i * f];
     for (int i = threadIdx.x; i < tw_hi_len(L1e); i += kThreads) sm.thi[i] = tw[(i << 6) * f];
   }
+  if (C > 1)
+    for (int e = threadIdx.x; e < C; e += kThreads) sm.twc[e] = tw[e * (P.twN / C)];
   if (sm.ctwe) {
+    // resident tables in the layouts of the staged column stage (cross_push): the four-step
+    // twiddle W_L^{r k1} of this CTA's row at the local DIF output slot p (k1 = dperm(p)) -- the
+    // sender applies it before the push, and the receiver's first inverse stage its conjugate --
+    // and the pair twiddles W_{2L}^{bin} of the a-side bins (k2a, column (i, 0)) at i C + k2a
     const int64_t n = P.n;
     const int twL_e = P.twN / int(n), twL_p = P.twN / int(n / 2);
-    const int nce = L1e / C, ncp = L1p / C;
-    for (int u = threadIdx.x; u < L1e; u += kThreads) {     // column twiddles W_L^{q k1}
-      const int q = u / nce, col = u - q * nce;
-      sm.ctwe[u] = tw[q * col_k1(L1e, C, r, col) * twL_e];
-    }
-    for (int u = threadIdx.x; u < L1p; u += kThreads) {
-      const int q = u / ncp, col = u - q * ncp;
-      sm.ctwp[u] = tw[q * col_k1(L1p, C, r, col) * twL_p];
-    }
-    // task-order slices of CTA r: index ((r C + k2) 2 + ab) np + i = r L1 + local
-    for (int u = threadIdx.x; u < L1e; u += kThreads) {
-      const int np = P.npe;
-      const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
-      sm.pwe[u] = tw[task_bin(L1e, C, int(r), i, k2, ab) * (P.twN / int(2 * n))];
-    }
-    for (int u = threadIdx.x; u < L1p; u += kThreads) {
-      const int np = P.npp;
-      const int i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
-      sm.pwp[u] = tw[task_bin(L1p, C, int(r), i, k2, ab) * (P.twN / int(n))];
-    }
+    const int lC = __ffs(C) - 1, l1e = __ffs(L1e) - 1, l1p = __ffs(L1p) - 1;
+    for (int u = threadIdx.x; u < L1e; u += kThreads) sm.ctwe[u] = tw[int(r) * dperm(u, l1e) * twL_e];
+    for (int u = threadIdx.x; u < L1p; u += kThreads) sm.ctwp[u] = tw[int(r) * dperm(u, l1p) * twL_p];
+    for (int u = threadIdx.x; u < L1e / 2; u += kThreads)
+      sm.pwe[u] = tw[task_bin(L1e, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(2 * n))];
+    for (int u = threadIdx.x; u < L1p / 2; u += kThreads)
+      sm.pwp[u] = tw[task_bin(L1p, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(n))];
   }
 }
 
@@ -636,6 +632,60 @@ __device__ __forceinline__ void local_fft_ct(double2 *A, const double2 *twd, int
   }
 }
 
+template <int L, int S>   // forward radix-4 stages S-1 .. 1 (all but the last), each followed by a barrier
+struct Ct4Top {
+  __device__ __forceinline__ static void run(double2 *A, const double2 *twd, int L1e) {
+    if constexpr (S > 1) {
+      st4_ct<false, 2 * S>(A, L, twd, L1e);
+      __syncthreads();
+      Ct4Top<L, S - 1>::run(A, twd, L1e);
+    }
+  }
+};
+// Last forward DIF stage (radix 4, m = 4, twiddle-free) handing its outputs to `out`.  Below
+// 4 kThreads points several threads share a butterfly (each loads it, pushes a subset of its
+// outputs), so every thread takes part in the push-in.
+template <int L, class OUT>
+__device__ __forceinline__ void last_stage_out(const double2 *A, const OUT &out) {
+  constexpr int NB = L / 4;
+  if constexpr (NB >= kThreads) {
+    for (int b = threadIdx.x; b < NB; b += kThreads) {
+      double2 a0 = A[pidx(4 * b)], a1 = A[pidx(4 * b + 1)], a2 = A[pidx(4 * b + 2)], a3 = A[pidx(4 * b + 3)];
+      bfly4<false>(a0, a1, a2, a3);
+      out(4 * b, a0); out(4 * b + 1, a1); out(4 * b + 2, a2); out(4 * b + 3, a3);
+    }
+  } else {
+    constexpr int R = kThreads / NB;
+    const int b = threadIdx.x % NB, h = threadIdx.x / NB;
+    if (h < 4) {
+      double2 a[4] = {A[pidx(4 * b)], A[pidx(4 * b + 1)], A[pidx(4 * b + 2)], A[pidx(4 * b + 3)]};
+      bfly4<false>(a[0], a[1], a[2], a[3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j % R == h) out(4 * b + j, a[j]);
+    }
+  }
+}
+
+// Forward compile-time FFT whose last DIF stage (radix 4, m = 4, twiddle-free) hands every output
+// slot to a functor instead of storing it (cross_push's push-in).  No trailing barrier.
+template <int L, class OUT>
+__device__ __forceinline__ void local_fft_ct_fwd_out(double2 *A, const double2 *twd, int L1e, const OUT &out) {
+  constexpr int l = __builtin_ctz(L), S4 = l / 2;
+  constexpr bool r2 = l & 1;
+  if constexpr (r2) {
+    for (int b = threadIdx.x; b < L / 2; b += kThreads) {
+      const int p0 = pidx(b), p1 = pidx(b + L / 2);
+      const double2 a0 = A[p0], a1 = A[p1];
+      A[p0] = cadd(a0, a1);
+      A[p1] = cmul(csub(a0, a1), twd[b * (L1e / L)]);
+    }
+    __syncthreads();
+  }
+  Ct4Top<L, S4>::run(A, twd, L1e);
+  last_stage_out<L>(A, out);
+}
+
 // Requires the input to be visible to all threads (caller synchronizes); ends synchronized.
 // Radix-4 stages are fused pairwise into radix-16 register passes from the bottom (stages
 // (1,0), (3,2), ...); a leftover top radix-4 stage and the radix-2 stage run alone.
@@ -705,7 +755,13 @@ __host__ __device__ constexpr int brev(int i) {
 // In-register radix-2 FFT of N <= 16 points: forward X_k = sum x_q W_N^{qk}; INV uses W^{-1}.
 template <int N, bool INV>
 __device__ __forceinline__ void fft_reg(double2 (&x)[N]) {
-  if constexpr (N > 1) {
+  if constexpr (N == 2) {
+    const double2 a = x[0];
+    x[0] = cadd(a, x[1]);
+    x[1] = csub(a, x[1]);
+  } else if constexpr (N == 4) {
+    bfly4<INV>(x[0], x[1], x[2], x[3]);     // natural-order 4-point DFT, no products by 0 / 1
+  } else if constexpr (N > 1) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const int j = brev<N>(i);
@@ -874,121 +930,294 @@ __device__ __forceinline__ int gslot(const Geo &g, int k1) {
   return ((k1 & ((1 << g.lr) - 1)) << g.ls) + dslot(k1 >> g.lr, g.ls);
 }
 
+// ------------------------------------------------------------------------ staged column stage
+// Thread split of the length-C column DFTs (C = T x Q): T lanes per column, Q points per lane,
+// a column PAIR (i, 0) / (i, 1) on G = 2T consecutive lanes, so both columns of every real-split
+// bin pair sit in one lane group and the whole stage runs in registers with shuffles.
+#ifndef TSF_COL_T16
+#define TSF_COL_T16 4      // lanes per column at C = 16 (4: 4 points per lane; 1: whole column)
+#endif
+template <int C> struct ColSplit {
+  static constexpr int T = C >= 16 ? TSF_COL_T16 : 1;   // C <= 8: a whole column per lane
+  static constexpr int Q = C / T;
+  static constexpr int G = 2 * T;
+  static constexpr int LT = T == 4 ? 2 : (T == 2 ? 1 : 0);
+  static constexpr int SH = 2 - LT;          // log2(8 / G): XOR key shift of the B swizzle
+};
+
+// Receive-buffer index of row q (source CTA) of column t = ab np + i.  The column stage reads,
+// per lane group, rows q = s + T m of both columns of pair i; the XOR key (s, ab) << SH spreads
+// the 8 lanes of each 16-byte-access phase over 8 distinct bank groups (np >= 8).
+template <int C>
+__device__ __forceinline__ int bix(int q, int t, int ncol, int lnp) {
+  using S = ColSplit<C>;
+  if (lnp < 3) return q * ncol + t;
+  const int key = ((q & (S::T - 1)) | (((t >> lnp) & 1) << S::LT)) << S::SH;
+  return q * ncol + (t ^ key);
+}
+
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int m, unsigned mask) {
+  return make_double2(__shfl_xor_sync(mask, v.x, m), __shfl_xor_sync(mask, v.y, m));
+}
+
+// x[k] *= W_C^{s k} (k < N compile-time slots, s < T runtime) from the SMEM table W_C^e
+template <int C, int N>
+__device__ __forceinline__ void twiddle_tab(double2 (&x)[N], int s, const double2 *twc) {
+#pragma unroll
+  for (int k = 1; k < N; ++k) x[k] = cmul(x[k], lds2(twc + ((s * k) & (C - 1))));
+}
+
+// In-group transposition (T lanes): lane s holds slots sigma; round b moves every slot whose
+// bit b differs from the lane's bit b to lane s ^ b, at slot sigma ^ b (an involution, so the
+// inverse runs the rounds in reverse order).
+template <int T, int Q>
+__device__ __forceinline__ void group_transpose(double2 (&x)[Q], int s, unsigned mask, bool rev) {
+#pragma unroll
+  for (int bi = 0; bi < 2; ++bi) {
+    const int b = rev ? (T >> 1) >> bi : 1 << bi;
+    if (b >= T || b == 0) continue;
+    const bool hi = s & b;
+#pragma unroll
+    for (int s0 = 0; s0 < Q; ++s0) {
+      if (s0 & b) continue;
+      const int s1 = s0 | b;
+      const double2 send = hi ? x[s0] : x[s1];
+      const double2 recv = shfl_xor2(send, b, mask);
+      if (hi) x[s0] = recv; else x[s1] = recv;
+    }
+  }
+}
+
+// Push of local DIF output slot p (bin k1 = dperm(p)) into row r of the B buffer of the CTA that
+// owns k1's column pair (cross_push); callable from the last forward FFT stage.
+template <int C>
+struct PushIn {
+  uint32_t bB, aB;
+  int L1, l1, np, ncol, lnp, r, twL;
+  const double2 *rt;                 // resident row twiddles W_L^{r k1} by slot, else nullptr
+  const double2 *tw;
+  __device__ __forceinline__ PushIn(double2 *B, uint64_t *mbB, const Geo &g, uint32_t rr, const double2 *tw_)
+      : bB(smem_u32(B)), aB(smem_u32(mbB)), L1(g.L1), l1(g.l1), np(g.np), ncol(g.L1 / C), lnp(g.lnp),
+        r(int(rr)), twL(g.twL), rt(g.ctw), tw(tw_) {}
+  // v times the four-step twiddle W_L^{r k1} of this row, pushed into the owner's B
+  __device__ __forceinline__ void operator()(int p, double2 v) const {
+    const int k1 = dperm(p, l1);
+    v = cmul(v, rt ? lds2(rt + p) : tw[r * k1 * twL]);
+    int pi, ab;
+    if (k1 == 0) { pi = 0; ab = 0; }
+    else if (k1 == L1 / 2) { pi = 0; ab = 1; }
+    else if (k1 < L1 / 2) { pi = k1; ab = 0; }
+    else { pi = L1 - k1; ab = 1; }
+    const uint32_t q = uint32_t(pi) & (C - 1);
+    const int idx = bix<C>(r, ab * np + pi / C, ncol, lnp);
+    push2(mapa_u32(bB + 16u * idx, q), v, mapa_u32(aB, q));
+  }
+};
+
+// Receiver's half of the four-step twiddle: slot p of O (bin k1 = dperm(p)) times conj W_L^{r k1}.
+__device__ __forceinline__ double2 orow(const Geo &g, uint32_t r, const double2 *tw, int p) {
+  return g.ctw ? lds2(g.ctw + p) : tw[int(r) * dperm(p, g.l1) * g.twL];
+}
+// First inverse (DIT) stage of a compile-time FFT (radix 4, m = 4, all twiddles 1) on the received
+// slots with the row twiddle applied on the way in; ends synchronized.
+template <int L>
+__device__ __forceinline__ void inv_first_fix(double2 *O, const Geo &g, uint32_t r, const double2 *tw) {
+  for (int b = threadIdx.x; b < L / 4; b += kThreads) {
+    double2 a0 = cmulc(O[pidx(4 * b)], orow(g, r, tw, 4 * b));
+    double2 a1 = cmulc(O[pidx(4 * b + 1)], orow(g, r, tw, 4 * b + 1));
+    double2 a2 = cmulc(O[pidx(4 * b + 2)], orow(g, r, tw, 4 * b + 2));
+    double2 a3 = cmulc(O[pidx(4 * b + 3)], orow(g, r, tw, 4 * b + 3));
+    bfly4<true>(a0, a1, a2, a3);
+    O[pidx(4 * b)] = a0; O[pidx(4 * b + 1)] = a1; O[pidx(4 * b + 2)] = a2; O[pidx(4 * b + 3)] = a3;
+  }
+  __syncthreads();
+}
+// Inverse radix-4 stages m = 2^LM .. 2^LMEND (each followed by a barrier)
+template <int L, int LM, int LMEND>
+struct Ct4InvFrom {
+  __device__ __forceinline__ static void run(double2 *A, const double2 *twd, int L1e) {
+    if constexpr (LM <= LMEND) {
+      st4_ct<true, LM>(A, L, twd, L1e);
+      __syncthreads();
+      Ct4InvFrom<L, LM + 2, LMEND>::run(A, twd, L1e);
+    }
+  }
+};
+// Inverse compile-time FFT of the received O: row twiddles in the first stage, then the rest
+template <int L>
+__device__ __forceinline__ void local_fft_ct_inv_fix(double2 *O, const Geo &g, uint32_t r, const double2 *tw,
+                                                     const double2 *twd, int L1e) {
+  constexpr int l = __builtin_ctz(L), S4 = l / 2;
+  inv_first_fix<L>(O, g, r, tw);
+  Ct4InvFrom<L, 4, 2 * S4>::run(O, twd, L1e);
+  if constexpr (l & 1) {
+    for (int b = threadIdx.x; b < L / 2; b += kThreads) {
+      const int p0 = pidx(b), p1 = pidx(b + L / 2);
+      const double2 a0 = O[p0];
+      const double2 a1 = cmulc(O[p1], twd[b * (L1e / L)]);
+      O[p0] = cadd(a0, a1);
+      O[p1] = csub(a0, a1);
+    }
+    __syncthreads();
+  }
+}
+
 // C > 1, staged: the four-step column stage through the receive buffer B and the output O,
-// both filled by pushes.  B layout: B[q * ncol + ab * np + i]
-// holds row q (source CTA q, bin k1 + L1 k2 after the column DFT) of this CTA's column
-// (i, ab), k1 = col_k1(i, ab).  Steps: push the local DIF output (slot p holds bin dperm(p)) to
-// the owner of its column pair; column DFT_C with twiddles W_L^{q k1}; per bin pair the real
-// split + spectral op; inverse column DFT, conjugate twiddles, push row q back to CTA q's O at
-// the slot of k1.  Returns with O complete and visible.
+// both filled by pushes.  Steps: push the local DIF output (slot
+// p holds bin dperm(p)) into row r of the owner's B (layout bix); per column pair, on its lane
+// group: column DFT_C (twiddles W_L^{q k1}, Q-point DFTs in registers, in-group transposition,
+// T-point DFTs), the real split + spectral op of every bin pair (k2, (i,0)) <-> (C-1-k2, (i,1))
+// with the partner lane (lane ^ (2T-1), slot Q-1-sigma), the inverse column DFT, conjugate
+// twiddles, and push row q back to CTA q's O at the slot of k1.  The pseudo column pair
+// (0, L1/2) of CTA 0 pairs bins inside each column and is redone by warp 0 through B.
+// Returns with O complete and visible.
 template <int C>
 __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, const Geo &g,
                                            const SpecOp &op, const double2 *__restrict__ tw, uint32_t r,
-                                           const Smem &sm, Xch &xs) {
+                                           const Smem &sm, Xch &xs, bool prepushed = false) {
+  using S = ColSplit<C>;
+  constexpr int T = S::T, Q = S::Q, G = S::G;
   TSF_PT0();
-  const int L1 = g.L1, l1 = g.l1, ncol = L1 / C, np = g.np;
+  const int L1 = g.L1, l1 = g.l1, ncol = L1 / C, np = g.np, lnp = g.lnp;
   uint64_t *mbB = sm.mbar, *mbO = sm.mbar + 1;
   const uint32_t ph = xs.nap & 1;
   if (threadIdx.x == 0) {
     mbar_expect(mbB, uint32_t(L1 * 16));
     mbar_expect(mbO, uint32_t(L1 * 16));
   }
-  {
-    const uint32_t bB = smem_u32(B), aB = smem_u32(mbB);
+  if (!prepushed) {
+    const PushIn<C> pin(B, mbB, g, r, tw);
 #pragma unroll 4
-    for (int p = threadIdx.x; p < L1; p += kThreads) {
-      const int k1 = dperm(p, l1);
-      int pi, ab;
-      if (k1 == 0) { pi = 0; ab = 0; }
-      else if (k1 == L1 / 2) { pi = 0; ab = 1; }
-      else if (k1 < L1 / 2) { pi = k1; ab = 0; }
-      else { pi = L1 - k1; ab = 1; }
-      const uint32_t q = uint32_t(pi) & (C - 1);
-      const int idx = int(r) * ncol + ab * np + pi / C;
-      push2(mapa_u32(bB + 16u * idx, q), A[pidx(p)], mapa_u32(aB, q));
-    }
+    for (int p = threadIdx.x; p < L1; p += kThreads) pin(p, A[pidx(p)]);
+  }
+  // pseudo column pair items of CTA 0 (warp 0, one pair per lane): twiddles prefetched
+  constexpr int NPS = C / 2 + 1 + (C + 1) / 2;
+  const int lane32 = threadIdx.x & 31;
+  double2 wps = make_double2(1.0, 0.0);
+  if (r == 0 && threadIdx.x < NPS) {
+    const bool c0 = lane32 <= C / 2;
+    const int k2 = c0 ? lane32 : lane32 - (C / 2 + 1);
+    const int bin = c0 ? L1 * k2 : L1 / 2 + L1 * k2;
+    wps = tw[bin * g.tw2L];
   }
   mbar_wait(mbB, ph);
   TSF_PACC(sm, PS_GATHER);
-  for (int t = threadIdx.x; t < ncol; t += kThreads) {        // column DFT_C
-    const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
+  const int lane = threadIdx.x & (G - 1), ab = lane >> S::LT, s = lane & (T - 1);
+  const unsigned gmask = ((1u << G) - 1u) << (lane32 & ~(G - 1));
+  const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
+  const int nsh = np * C;                     // offset of the b-side multipliers (SMEM layout)
+  const bool msh = op.mul != nullptr && op.mul_sh;   // per-level table in SMEM (B forms lambda)
+  for (int i = threadIdx.x / G; i < np; i += kThreads / G) {
+    const int t = ab * np + i, colo = 2 * i + ab;
     const int k1 = col_k1(L1, C, r, colo);
-    double2 z[C];
-#pragma unroll
-    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
-    if (g.ctw) {
-#pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], g.ctw[q * ncol + colo]);
-    } else {
-#pragma unroll
-      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
-    }
-    fft_reg<C, false>(z);
-#pragma unroll
-    for (int q = 0; q < C; ++q) B[q * ncol + t] = z[q];
-  }
-  __syncthreads();
-  TSF_PACC(sm, PS_COLF);
-  // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1)).
-  // The pseudo column pair (0, L1/2) of CTA 0 is done afterwards by warp 0, one pair per lane:
-  // inside the item loop its branch diverged from the regular lanes in every warp and made
-  // CTA 0's stage ~2.4x longer than its peers' (measured), which all of them then waited for.
-  for (int u = threadIdx.x; u < np * C; u += kThreads) {
-    const int k2 = u >> g.lnp, i = u & (np - 1);
     const int pi = int(r) + i * C;
-    if (pi == 0) continue;
-    const int bin = pi + L1 * k2;
-    double2 &za = B[k2 * ncol + i];
-    double2 &zb = B[(C - 1 - k2) * ncol + np + i];
-    double2 a = za, b = zb;
-    pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
-               op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
-    za = a;
-    zb = b;
-  }
-  if (r == 0 && threadIdx.x < C / 2 + 1 + (C + 1) / 2) {
-    // one bin pair per lane, branch-free (operands selected, a single pair_apply):
-    // column 0 (bins L1 k2): k2 <-> (C - k2) mod C, k2 = 0 with the Nyquist bin;
-    // column L1/2 (bins L1/2 + L1 k2): k2 <-> C - 1 - k2
-    const int o = threadIdx.x;
-    const bool c0 = o <= C / 2;
-    const int k2 = c0 ? o : o - (C / 2 + 1);
-    const int kp = c0 ? (C - k2) % C : C - 1 - k2;
-    const int ab = c0 ? 0 : 1;
-    const int cof = c0 ? 0 : np;
-    const int bin = c0 ? L1 * k2 : L1 / 2 + L1 * k2;
-    const bool self = kp == k2;
-    const double2 la = op.get(k2, ab, 0, bin);
-    const double2 lp = op.get(kp, ab, 0, g.L - bin);
-    const double2 lb = self ? ((c0 && k2 == 0) ? op.nyqe : la) : lp;
-    const double2 w = op.wtw(k2, ab, 0, bin, tw, g.tw2L);
-    double2 &za = B[k2 * ncol + cof];
-    double2 a = za, b = self ? za : B[kp * ncol + cof];
-    pair_apply(a, b, la, lb, w, op.scale);
-    za = a;
-    if (!self) B[kp * ncol + cof] = b;
-  }
-  __syncthreads();
-  TSF_PACC(sm, PS_PAIRS);
-  {
-    const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
-    for (int t = threadIdx.x; t < ncol; t += kThreads) {      // inverse column DFT_C + push back
-      const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
-      const int k1 = col_k1(L1, C, r, colo);
-      double2 z[C];
+    double2 x[Q];
 #pragma unroll
-      for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
-      fft_reg<C, true>(z);
-      if (g.ctw) {
+    for (int m = 0; m < Q; ++m) {             // column DFT_C, rows q = s + T m
+      x[m] = B[bix<C>(s + T * m, t, ncol, lnp)];   // row twiddles applied by the sender
+    }
+    fft_reg<Q, false>(x);
+    if constexpr (T > 1) twiddle_tab<C, Q>(x, s, sm.twc);
+    group_transpose<T, Q>(x, s, gmask, false);
 #pragma unroll
-        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], g.ctw[q * ncol + colo]);
-      } else {
+    for (int j = 0; j < Q / T; ++j) {         // slot j T + kb holds bin k2 = s + T j + Q kb
+      double2 y[T];
 #pragma unroll
-        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      for (int kb = 0; kb < T; ++kb) y[kb] = x[j * T + kb];
+      fft_reg<T, false>(y);
+#pragma unroll
+      for (int kb = 0; kb < T; ++kb) x[j * T + kb] = y[kb];
+    }
+    const bool pseudo = (r == 0) && (i == 0);
+    if (pseudo) {                             // pre-pair values for warp 0's pseudo pass
+#pragma unroll
+      for (int sg = 0; sg < Q; ++sg) B[bix<C>(s + T * (sg / T) + Q * (sg % T), t, ncol, lnp)] = x[sg];
+    }
+    {                                         // regular bin pairs with the partner lane
+      double2 y[Q / 2];
+#pragma unroll
+      for (int jj = 0; jj < Q / 2; ++jj) y[jj] = shfl_xor2(x[Q - 1 - jj], G - 1, gmask);
+#pragma unroll
+      for (int jj = 0; jj < Q / 2; ++jj) {
+        const int k2m = s + T * (jj / T) + Q * (jj % T);
+        const int k2a = ab ? C - 1 - k2m : k2m;
+        const int bin = pi + L1 * k2a;
+        double2 la, lb, w;
+        if (msh) {
+          la = lds2(op.mul + i * C + k2a);
+          lb = lds2(op.mul + nsh + i * C + k2a);
+          if (op.conj) { la = cconj(la); lb = cconj(lb); }
+        } else {
+          la = op.get(k2a, 0, i, bin);
+          lb = op.get(C - 1 - k2a, 1, i, g.L - bin);
+        }
+        w = op.pw ? lds2(op.pw + i * C + k2a) : tw[bin * g.tw2L];
+        double2 a = ab ? y[jj] : x[jj], b = ab ? x[jj] : y[jj];
+        pair_apply(a, b, la, lb, w, op.scale);
+        x[jj] = ab ? b : a;
+        y[jj] = ab ? a : b;
       }
-      const uint32_t dst = bO + 16u * uint32_t(pidx(dslot(k1, l1)));
 #pragma unroll
-      for (int q = 0; q < C; ++q) push2(mapa_u32(dst, uint32_t(q)), z[q], mapa_u32(aO, uint32_t(q)));
+      for (int jj = 0; jj < Q / 2; ++jj) x[Q - 1 - jj] = shfl_xor2(y[jj], G - 1, gmask);
+    }
+    if (r == 0 && threadIdx.x < 32 && i < 32 / G) {
+      // warp 0, first pass: the pseudo column pair (0, L1/2), one bin pair per lane, branch-free:
+      // column 0 (bins L1 k2): k2 <-> (C - k2) mod C, k2 = 0 with the Nyquist bin; column L1/2
+      // (bins L1/2 + L1 k2): k2 <-> C - 1 - k2
+      const int nact = np * G >= 32 ? 32 : np * G;
+      const unsigned am = nact >= 32 ? 0xffffffffu : ((1u << nact) - 1u);
+      __syncwarp(am);
+      for (int o = lane32; o < NPS; o += nact) {
+        const bool c0 = o <= C / 2;
+        const int k2 = c0 ? o : o - (C / 2 + 1);
+        const int kp = c0 ? (C - k2) % C : C - 1 - k2;
+        const int abp = c0 ? 0 : 1;
+        const int cof = c0 ? 0 : np;
+        const int bin = c0 ? L1 * k2 : L1 / 2 + L1 * k2;
+        const bool self = kp == k2;
+        double2 la, lp;
+        if (msh) {
+          la = lds2(op.mul + (abp ? nsh + (C - 1 - k2) : k2));
+          lp = lds2(op.mul + (abp ? nsh + (C - 1 - kp) : kp));
+          if (op.conj) { la = cconj(la); lp = cconj(lp); }
+        } else {
+          la = op.get(k2, abp, 0, bin);
+          lp = op.get(kp, abp, 0, g.L - bin);
+        }
+        const double2 lb = self ? ((c0 && k2 == 0) ? op.nyqe : la) : lp;
+        const double2 w = o == lane32 ? wps : tw[bin * g.tw2L];
+        double2 &za = B[bix<C>(k2, cof, ncol, lnp)];
+        double2 a = za, b = self ? za : B[bix<C>(kp, cof, ncol, lnp)];
+        pair_apply(a, b, la, lb, w, op.scale);
+        za = a;
+        if (!self) B[bix<C>(kp, cof, ncol, lnp)] = b;
+      }
+      __syncwarp(am);
+      if (pseudo) {
+#pragma unroll
+        for (int sg = 0; sg < Q; ++sg) x[sg] = B[bix<C>(s + T * (sg / T) + Q * (sg % T), t, ncol, lnp)];
+      }
+    }
+    // inverse column DFT_C: T-point inverse DFTs over kb, W_C^{-s' ka}, transposition back,
+    // Q-point inverse DFTs -> row q = s + T m at slot m
+#pragma unroll
+    for (int j = 0; j < Q / T; ++j) {
+      double2 y[T];
+#pragma unroll
+      for (int kb = 0; kb < T; ++kb) y[kb] = x[j * T + kb];
+      fft_reg<T, true>(y);
+      // slot j T + s' times W_C^{-s' (j T + s)}
+      x[j * T] = y[0];
+#pragma unroll
+      for (int sp = 1; sp < T; ++sp) x[j * T + sp] = cmulc(y[sp], lds2(sm.twc + ((sp * (j * T + s)) & (C - 1))));
+    }
+    group_transpose<T, Q>(x, s, gmask, true);
+    fft_reg<Q, true>(x);
+    const uint32_t dst = bO + 16u * uint32_t(pidx(dslot(k1, l1)));
+#pragma unroll
+    for (int m = 0; m < Q; ++m) {             // the receiver applies conj W_L^{q k1} (ofix)
+      const int q = s + T * m;
+      push2(mapa_u32(dst, uint32_t(q)), x[m], mapa_u32(aO, uint32_t(q)));
     }
   }
   TSF_PACC(sm, PS_COLI);
@@ -1268,7 +1497,23 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
                                             const double2 *__restrict__ tw, uint32_t r, Xch &xs,
                                             double2 *xg) {
   TSF_PT0();
-  local_fft<false>(sm.A, g.L1, sm, L1e);
+  bool pre = false;               // forward FFT already pushed its outputs (staged, compile-time FFT)
+  if constexpr (C > 1 && STG) {
+#ifndef TSF_NO_CT_FFT
+    if (sm.twd != nullptr && L1e == 1024 && (g.L1 == 1024 || g.L1 == 512)) {
+      const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+      if (g.L1 == 1024) local_fft_ct_fwd_out<1024>(sm.A, sm.twd, L1e, pin);
+      else local_fft_ct_fwd_out<512>(sm.A, sm.twd, L1e, pin);
+      pre = true;
+    } else if (sm.twd != nullptr && L1e == 256 && (g.L1 == 256 || g.L1 == 128)) {
+      const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+      if (g.L1 == 256) local_fft_ct_fwd_out<256>(sm.A, sm.twd, L1e, pin);
+      else local_fft_ct_fwd_out<128>(sm.A, sm.twd, L1e, pin);
+      pre = true;
+    }
+#endif
+  }
+  if (!pre) local_fft<false>(sm.A, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_F);
   double2 *Y = sm.A;
   if constexpr (C == 1) {
@@ -1277,7 +1522,7 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
     TSF_PACC(sm, PS_PAIRS);
   } else {
     if constexpr (STG) {
-      cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs);
+      cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs, pre);
       Y = sm.O;
     } else {
       for (int p = threadIdx.x; p < g.L1; p += kThreads) __stcg(xg + int64_t(r) * g.L1 + p, sm.A[pidx(p)]);
@@ -1297,7 +1542,24 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
     }
     TSF_PTR();
   }
-  local_fft<true>(Y, g.L1, sm, L1e);
+  if constexpr (C > 1 && STG) {
+    // O still lacks the receiver's row twiddles conj W_L^{r k1}: in the first stage of the
+    // compile-time inverse FFTs, else one pass
+    bool done = false;
+#ifndef TSF_NO_CT_FFT
+    if (sm.twd != nullptr && L1e == 1024 && g.L1 == 1024) { local_fft_ct_inv_fix<1024>(Y, g, r, tw, sm.twd, L1e); done = true; }
+    else if (sm.twd != nullptr && L1e == 1024 && g.L1 == 512) { local_fft_ct_inv_fix<512>(Y, g, r, tw, sm.twd, L1e); done = true; }
+    else if (sm.twd != nullptr && L1e == 256 && g.L1 == 256) { local_fft_ct_inv_fix<256>(Y, g, r, tw, sm.twd, L1e); done = true; }
+    else if (sm.twd != nullptr && L1e == 256 && g.L1 == 128) { local_fft_ct_inv_fix<128>(Y, g, r, tw, sm.twd, L1e); done = true; }
+#endif
+    if (!done) {
+      for (int p = threadIdx.x; p < g.L1; p += kThreads) Y[pidx(p)] = cmulc(Y[pidx(p)], orow(g, r, tw, p));
+      __syncthreads();
+      local_fft<true>(Y, g.L1, sm, L1e);
+    }
+  } else {
+    local_fft<true>(Y, g.L1, sm, L1e);
+  }
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
@@ -1394,20 +1656,35 @@ __device__ __forceinline__ void fill_mul(const DevParams &P, const Inst &I, int6
   SpecOp a = make_op(P, I, j, OP_A, r, none), pinv = make_op(P, I, j, OP_PINV, r, none);
   const bool res = sm.mule != nullptr;
   const int L1e = P.L1e, L1p = P.L1p, C = P.C;
+  // resident (SMEM) tables in the staged column stage's layout: a-side bins (k2a, column (i, 0))
+  // at i C + k2a, b-side bins (C-1-k2a, column (i, 1)) at np C + i C + k2a; the HBM tables in
+  // task order
+  const int lC = __ffs(C) - 1;
+  auto slot_task = [&](int u, int np, int &k2, int &ab, int &i) {
+    const int lnp = __ffs(np) - 1;
+    if (res) {
+      ab = u >> (lnp + lC);
+      const int k2a = u & (C - 1);
+      i = (u >> lC) & (np - 1);
+      k2 = ab ? C - 1 - k2a : k2a;
+    } else {
+      i = u & (np - 1); ab = (u >> lnp) & 1; k2 = u >> (lnp + 1);
+    }
+  };
   for (int u = threadIdx.x; u < L1e; u += kThreads) {
-    const int64_t g = int64_t(r) * L1e + u;
-    const double2 v = a.lam_idx(int(g), 0);
-    if (res) sm.mule[u] = v; else I.mul[g] = v;
+    int k2, ab, i;
+    slot_task(u, P.npe, k2, ab, i);
+    const double2 v = a.lam_idx(int(task_index(C, P.npe, int(r), k2, ab, i)), 0);
+    if (res) sm.mule[u] = v; else I.mul[int64_t(r) * L1e + u] = v;
   }
   if (P.precond == TSF_NOPREC) return;
   const int np = P.npp;
   for (int u = threadIdx.x; u < L1p; u += kThreads) {
-    const int64_t g = int64_t(r) * L1p + u;
-    const int lnp = __ffs(np) - 1;
-    const int i = u & (np - 1), ab = (u >> lnp) & 1, k2 = u >> (lnp + 1);
+    int k2, ab, i;
+    slot_task(u, np, k2, ab, i);
     const int bin = int(task_bin(L1p, C, int(r), i, k2, ab));
-    const double2 v = pinv.eff(pinv.lam_idx(int(g), bin));
-    if (res) sm.mulp[u] = v; else I.mul[P.n + g] = v;
+    const double2 v = pinv.eff(pinv.lam_idx(int(task_index(C, np, int(r), k2, ab, i)), bin));
+    if (res) sm.mulp[u] = v; else I.mul[P.n + int64_t(r) * L1p + u] = v;
   }
 }
 
@@ -1812,6 +2089,186 @@ __device__ __forceinline__ void gsf_level(const DevParams &P, const Inst &I, con
 // a single state machine for everything cost ~6% at C3 against this shape.
 enum LevelState { S_RHS = 0, S_WARM = 1, S_TRUE = 2, S_KRYLOV = 3 };
 
+// ------------------------------------------------------------------------ fused BiCGSTAB (C3 shape)
+// For the C3 geometry (C = 16 CTAs, local lengths L1e = 1024 / L1p = 512, staged exchange,
+// resident twiddles) the first forward and the last inverse radix stage of every application
+// touch exactly the elements e = tid, tid + 256 that thread tid owns in the vector loops.  The
+// BiCGSTAB vector updates therefore ride on those stages: the update that produces an
+// application's input feeds its first stage from registers, the last stage of P^{-1} feeds the
+// first stage of A directly (phat / shat are only stored for the x update), and the last stage
+// of A yields v / t with their dot products.  Same arithmetic and summation order as the
+// unfused loop (R-fuse); one barrier and one shared-memory round trip fewer per stage boundary.
+namespace fz {
+constexpr int kH = kThreads;        // e = b and b + kH (npc = 512)
+// P^{-1} forward, first stage (radix 2, L = 512, twiddle W_512^b = twd[2b])
+__device__ __forceinline__ void p_first(double2 *A, int b, double2 a0, double2 a1, const double2 *twd) {
+  A[pidx(b)] = cadd(a0, a1);
+  A[pidx(b + kH)] = cmul(csub(a0, a1), twd[2 * b]);
+}
+// A forward, first stage (radix 4, m = 1024) on the zero-padded input (a2 = a3 = 0)
+__device__ __forceinline__ void a_first(double2 *A, int b, double2 a0, double2 a1, const double2 *twd) {
+  double2 a2 = zero2(), a3 = zero2();
+  const double2 w1 = twd[b];
+  const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+  bfly4<false>(a0, a1, a2, a3);
+  a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
+  A[pidx(b)] = a0; A[pidx(b + kH)] = a1; A[pidx(b + 2 * kH)] = a2; A[pidx(b + 3 * kH)] = a3;
+}
+// P^{-1} inverse, last stage (radix 2): elements b, b + 256
+__device__ __forceinline__ void p_last(const double2 *O, int b, const double2 *twd, double2 &o0, double2 &o1) {
+  const double2 a0 = O[pidx(b)];
+  const double2 a1 = cmulc(O[pidx(b + kH)], twd[2 * b]);
+  o0 = cadd(a0, a1);
+  o1 = csub(a0, a1);
+}
+// A inverse, last stage (radix 4, m = 1024): the kept (unpadded) elements b, b + 256
+__device__ __forceinline__ void a_last(const double2 *O, int b, const double2 *twd, double2 &o0, double2 &o1) {
+  double2 a0 = O[pidx(b)], a1 = O[pidx(b + kH)], a2 = O[pidx(b + 2 * kH)], a3 = O[pidx(b + 3 * kH)];
+  const double2 w1 = twd[b];
+  const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+  a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
+  bfly4<true>(a0, a1, a2, a3);
+  o0 = a0;
+  o1 = a1;
+}
+}  // namespace fz
+
+// One operator application after its first forward stage (caller: stage written, then barrier):
+// the remaining forward stages with the push-in fused into the last, the column stage, and the
+// inverse stages but the last (its caller does it).
+template <int C, int L>
+__device__ __forceinline__ void apply_mid(const Smem &sm, const Geo &g, const SpecOp &op,
+                                          const double2 *__restrict__ tw, uint32_t r, Xch &xs) {
+  TSF_PT0();
+  const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+  Ct4Top<L, 4>::run(sm.A, sm.twd, 1024);
+  last_stage_out<L>(sm.A, pin);
+  TSF_PACC(sm, PS_FFT_F);
+  cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs, true);
+  TSF_PTR();
+  inv_first_fix<L>(sm.O, g, r, tw);
+  Ct4InvFrom<L, 4, 8>::run(sm.O, sm.twd, 1024);
+  TSF_PACC(sm, PS_FFT_I);
+#ifdef TSF_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
+#endif
+}
+
+// The BiCGSTAB iterations of level_solve (default variant: x0 given by R/PV/RH/X, four reductions
+// merged to three: ||s||^2 travels with t.s and t.t, the half-step exit test follows them).
+// Half iteration hh = 0 (p -> phat -> v) and hh = 1 (s -> shat -> t) share ONE site of each
+// application (instruction-cache footprint); their vector work is dispatched on hh.
+template <int C>
+__device__ __forceinline__ void bicg_fused(const DevParams &P, const Smem &sm, const Vecs &V, const Geo &ge,
+                                           const Geo &gp, const SpecOp &opA, const SpecOp &opP,
+                                           const double2 *__restrict__ tw, uint32_t r, Xch &xs, double rr0,
+                                           double rn0, int &hs, double &relres, int &status) {
+  using namespace fz;
+  double2 *__restrict__ X = V.X, *__restrict__ R = V.R, *__restrict__ RH = V.RH, *__restrict__ PV = V.P;
+  double2 *__restrict__ VV = V.V, *__restrict__ S = V.S, *__restrict__ PH = V.PH, *__restrict__ SH = V.SH;
+  const double2 *twd = sm.twd;
+  double2 *A = sm.A, *O = sm.O;
+  const int b = threadIdx.x, b1 = threadIdx.x + kH;
+  double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0, ssp = 0.0;
+  double2 v0 = zero2(), v1 = zero2();
+  bool first = true;
+  for (;;) {
+#pragma unroll 1
+    for (int hh = 0; hh < 2; ++hh) {
+      TSF_PT0();
+      double2 i0, i1;             // input of P^{-1}: p (first iteration: r0) or s = r - alpha v
+      if (hh == 0) {
+        if (first) {
+          i0 = PV[b]; i1 = PV[b1];
+        } else {
+          i0 = caxpy(beta, caxpy(-omega, VV[b], PV[b]), R[b]);
+          i1 = caxpy(beta, caxpy(-omega, VV[b1], PV[b1]), R[b1]);
+          PV[b] = i0; PV[b1] = i1;
+        }
+      } else {
+        i0 = caxpy(-alpha, v0, R[b]);
+        i1 = caxpy(-alpha, v1, R[b1]);
+        S[b] = i0; S[b1] = i1;
+        ssp = 0.0;
+        ssp += cdot(i0, i0);
+        ssp += cdot(i1, i1);
+      }
+      __syncthreads();            // every thread done with A / O of the last application
+      p_first(A, b, i0, i1, twd);
+      TSF_PACC(sm, PS_VEC);
+      __syncthreads();
+      apply_mid<C, 512>(sm, gp, opP, tw, r, xs);
+      TSF_PTR();
+      {                           // phat / shat, and the first stage of A on it
+        double2 o0, o1;
+        p_last(O, b, twd, o0, o1);
+        double2 *H = hh == 0 ? PH : SH;
+        H[b] = o0; H[b1] = o1;
+        a_first(A, b, o0, o1, twd);
+      }
+      TSF_PACC(sm, PS_VEC);
+      __syncthreads();
+      apply_mid<C, 1024>(sm, ge, opA, tw, r, xs);
+      TSF_PTR();
+      double2 y0, y1;
+      a_last(O, b, twd, y0, y1);
+      if (hh == 0) {              // v; alpha = rho / (r^.v)
+        v0 = y0; v1 = y1;
+        VV[b] = y0; VV[b1] = y1;
+        double d[1] = {0.0};
+        d[0] += cdot(RH[b], y0);
+        d[0] += cdot(RH[b1], y1);
+        TSF_PACC(sm, PS_VEC);
+        csum<C, 1>(d, sm, xs);
+        if (!(fabs(d[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; return; }
+        alpha = rho / d[0];
+        continue;
+      }
+      // t: omega = t.s / t.t (with ||s||^2 in the same reduction); x, r updates
+      double tt[3] = {0.0, 0.0, ssp};
+      const double2 s0 = S[b], s1 = S[b1];
+      tt[0] += cdot(y0, s0);
+      tt[1] += cdot(y0, y0);
+      tt[0] += cdot(y1, s1);
+      tt[1] += cdot(y1, y1);
+      TSF_PACC(sm, PS_VEC);
+      csum<C, 3>(tt, sm, xs);
+      TSF_PTR();
+      if (sqrt(tt[2]) < P.tol * rn0) {        // half-step exit on ||s||
+        X[b] = caxpy(alpha, PH[b], X[b]);
+        X[b1] = caxpy(alpha, PH[b1], X[b1]);
+        hs += 1;
+        relres = sqrt(tt[2]) / rn0;
+        return;
+      }
+      if (!(tt[1] > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; return; }
+      omega = tt[0] / tt[1];
+      double rr[2] = {0.0, 0.0};
+      X[b] = caxpy(omega, SH[b], caxpy(alpha, PH[b], X[b]));
+      const double2 r0 = caxpy(-omega, y0, s0);
+      R[b] = r0;
+      rr[0] += cdot(RH[b], r0);
+      rr[1] += cdot(r0, r0);
+      X[b1] = caxpy(omega, SH[b1], caxpy(alpha, PH[b1], X[b1]));
+      const double2 r1 = caxpy(-omega, y1, s1);
+      R[b1] = r1;
+      rr[0] += cdot(RH[b1], r1);
+      rr[1] += cdot(r1, r1);
+      TSF_PACC(sm, PS_VEC);
+      csum<C, 2>(rr, sm, xs);
+      hs += 2;
+      relres = sqrt(rr[1]) / rn0;
+      if (!isfinite(relres)) { status = TSF_LEVEL_DIVERGED; return; }
+      if (relres < P.tol) return;
+      if (hs >= 2 * P.maxit) { status = TSF_LEVEL_MAXIT; return; }
+      if (!(fabs(rr[0]) > 1e-300)) { status = TSF_LEVEL_BREAKDOWN; return; }
+      beta = (rr[0] / rho) * (alpha / omega);
+      rho = rr[0];
+      first = false;
+    }
+  }
+}
+
 template <int C, int METHOD, bool STG, bool BIG>
 __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, const Smem &sm, const Vecs &V,
                                             int64_t j, uint32_t r, Xch &xs, int mode = 0, int64_t j0 = 0) {
@@ -1933,7 +2390,15 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
     relres = rn0 > 0.0 ? sqrt(rr0) / rn0 : 0.0;
     const bool iterate = rr0 > 0.0 && !(warm && sqrt(rr0) < P.tol * rn0);
 
-    if (iterate && (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF)) {
+    bool fused = false;
+    if constexpr (METHOD == TSF_BICGSTAB && C == 16 && STG && !BIG) {
+      if (iterate && P.fuse && prec && !P.pipelined && sm.twd != nullptr && sm.vs != nullptr &&
+          P.L1e == 1024 && P.L1p == 512) {
+        bicg_fused<C>(P, sm, V, ge, gp, opA, opP, tw, r, xs, rr0, rn0, hs, relres, status);
+        fused = true;
+      }
+    }
+    if (!fused && iterate && (METHOD == TSF_BICGSTAB || METHOD == TSF_GSF)) {
       // One BiCGSTAB iteration = four operator applications, h = 0..3: phat = P^{-1} p,
       // v = A phat, shat = P^{-1} s, t = A shat.  They go through ONE inlined apply (the operator
       // and geometry are selected per h) so the hot loop's code stays small for the instruction

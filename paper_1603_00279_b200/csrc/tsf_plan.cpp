@@ -151,6 +151,7 @@ int make_plan(const tsf_problem *p, int32_t B, const tsf_solver *s, Plan *pl) {
   P.x0_warm = s->x0_warm ? 1 : 0;
   P.true_res = s->true_residual ? 1 : 0;
   P.pipelined = s->pipelined ? 1 : 0;
+  if (const char *ef = std::getenv("TSF_NO_FUSE")) P.fuse = std::atoi(ef) ? 0 : 1;
   P.hblock = s->hist_block;
   const int64_t n = P.n;
   int C = s->cluster;
@@ -380,6 +381,7 @@ DevParams dev_params(const Plan &pl, char *ws) {
   d.x0_warm = pl.x0_warm;
   d.true_res = pl.true_res;
   d.pipelined = pl.pipelined;
+  d.fuse = pl.fuse;
   d.hblock = pl.hblock; d.o_hb = pl.o_hb; d.o_mul = pl.o_mul; d.o_gsf = pl.o_gsf; d.o_xg = pl.o_xg;
   return d;
 }

@@ -68,6 +68,7 @@ struct DevParams {
   int32_t true_res;                // compute ||g - A u^{j+1}|| / ||g|| at every level exit
   int32_t pipelined;               // NEXT-3: BiCGSTAB with two cluster reductions per iteration
   int32_t hblock;                  // NEXT-3: blocked history sum, block length (0 = direct)
+  int32_t fuse;                    // fused BiCGSTAB vector updates on the first/last FFT stages (C3 shape)
   int64_t o_hb;                    // blocked history: partial sums of the block's levels [hblock][n]
 };
 
@@ -90,6 +91,7 @@ struct Plan {
   size_t off_level = 0, off_prof = 0, off_scratch = 0, scratch_bytes = 0, off_inst = 0;
   size_t off_sync = 0, off_pre = 0, off_fptr = 0;
   int32_t x0_warm = 0, true_res = 0, pipelined = 0, hblock = 0;
+  int32_t fuse = 1;          // developer knob TSF_NO_FUSE=1 disables (bitwise A/B test)
   int64_t o_hb = 0;
   int32_t scratch_batch = 0;
   size_t stride = 0, total = 0;
@@ -165,7 +167,7 @@ TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resid
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;
   if (!staged) c2 += chunk_cplx;                   // chunk buffer of the unstaged column stage
-  int64_t d = 48 + 128 + 4 + 2;                    // reductions, push buffers, mbarriers, flag
+  int64_t d = 48 + 128 + 4 + 2 + 32;               // reductions, push buffers, mbarriers, flag, W_C table
   return 16 * c2 + 8 * d + 64;
 }
 

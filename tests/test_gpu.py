@@ -281,6 +281,34 @@ def test_history_helper_clusters_match_the_solver_own_history_bitwise(method, cl
     assert np.linalg.norm(outs[0][0] - Uo[-1]) <= RTOL * np.linalg.norm(Uo[-1])
 
 
+@pytest.mark.parametrize("src,pipelined", [("table", False), ("mms3", False), ("table", True)])
+def test_fused_bicgstab_c3_shape_equals_unfused_bitwise(src, pipelined, monkeypatch):
+    """C3 geometry (n = 2^14 on 16 CTAs): the fused BiCGSTAB loop (vector updates on the first /
+    last FFT stages, push-in fused into the last forward stage, DESIGN.md R-fuse) keeps the
+    unfused loop's arithmetic and summation order, so solutions and iteration counts are equal bit
+    for bit (TSF_NO_FUSE=1 runs the unfused loop).  The pipelined variant is never fused (same
+    result either way)."""
+    n, M = 16384, 6
+    f = np.random.default_rng(11).standard_normal((M, n)) if src == "table" else None
+    inst, _ = pair(0.9, 1.9, n, M, gamma=(O.CONST, 1.0), dplus=(O.CONST, 2.0), dminus=(O.CONST, 0.5),
+                   src=src, f_table=f)
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("TSF_NO_FUSE", "1")
+        s = tsf.Solver([inst], cluster=16, pipelined=pipelined)
+        U = run_levels(s, M)[0]
+        s.reset()
+        s.solve()
+        assert s.sync() == 0
+        np.testing.assert_array_equal(U[-1], s.solution(0))
+        outs.append((U, s.stats()[0].copy()))
+        s.close()
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    assert (outs[0][1] > 0).all()
+
+
 def test_next4_spectrum_export_matches_oracle_and_clusters_at_one(tmp_path):
     """NEXT-4 (Figs. fig1/fig2): the dense level matrix assembled from the GPU operator
     equals the oracle's, and the Strang-preconditioned spectrum is clustered at 1 with "about

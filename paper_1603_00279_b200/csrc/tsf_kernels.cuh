@@ -292,6 +292,19 @@ __device__ __forceinline__ double2 twid(const Smem &sm, int e) {
 __device__ __forceinline__ int col_k1(int L1, int C, uint32_t r, int col);
 __device__ __forceinline__ int dperm(int p, int l);
 
+#ifndef TSF_COL_T16
+#define TSF_COL_T16 4      // lanes per column at C = 16 (4: 4 points per lane; 1: whole column)
+#endif
+// Resident column twiddle W_L^{q k1} of column (i, ab), row q, in the order the lane groups of
+// the staged column stage read them (T = 4: the 8 lanes of a 16-byte phase are one group, rows
+// s + 4m of both columns; T = 1: four groups, one row).
+template <int C>
+__device__ __forceinline__ int ctw_idx(int q, int i, int ab, int np) {
+  if constexpr (C >= 16 && TSF_COL_T16 == 4) return (i * C + q) * 2 + ab;
+  else if constexpr (C >= 16) return (q * np + i) * 2 + ab;
+  else return q * (2 * np) + 2 * i + ab;          // C < 16: [q][column 2i+ab] (cross_push)
+}
+
 // Kernel prologue: local-FFT twiddles and (resident mode) this CTA's constant tables, copied
 // from the accurate global tables (twiddles tw[x] = exp(-2 pi i x / twN)).
 __device__ __forceinline__ void load_constants(const DevParams &P, const double2 *lwe, const double2 *lwp,
@@ -308,19 +321,37 @@ __device__ __forceinline__ void load_constants(const DevParams &P, const double2
   if (C > 1)
     for (int e = threadIdx.x; e < C; e += kThreads) sm.twc[e] = tw[e * (P.twN / C)];
   if (sm.ctwe) {
-    // resident tables in the layouts of the staged column stage (cross_push): the four-step
-    // twiddle W_L^{r k1} of this CTA's row at the local DIF output slot p (k1 = dperm(p)) -- the
-    // sender applies it before the push, and the receiver's first inverse stage its conjugate --
-    // and the pair twiddles W_{2L}^{bin} of the a-side bins (k2a, column (i, 0)) at i C + k2a
+    // resident tables in the layouts of the staged column stage (cross_push): column twiddles
+    // W_L^{q k1} at ctw_idx(q, i, ab), pair twiddles W_{2L}^{bin} of the a-side bins
+    // (k2a, column (i, 0)) at i C + k2a
     const int64_t n = P.n;
     const int twL_e = P.twN / int(n), twL_p = P.twN / int(n / 2);
-    const int lC = __ffs(C) - 1, l1e = __ffs(L1e) - 1, l1p = __ffs(L1p) - 1;
-    for (int u = threadIdx.x; u < L1e; u += kThreads) sm.ctwe[u] = tw[int(r) * dperm(u, l1e) * twL_e];
-    for (int u = threadIdx.x; u < L1p; u += kThreads) sm.ctwp[u] = tw[int(r) * dperm(u, l1p) * twL_p];
-    for (int u = threadIdx.x; u < L1e / 2; u += kThreads)
-      sm.pwe[u] = tw[task_bin(L1e, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(2 * n))];
-    for (int u = threadIdx.x; u < L1p / 2; u += kThreads)
-      sm.pwp[u] = tw[task_bin(L1p, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(n))];
+    const int lC = __ffs(C) - 1;
+    for (int u = threadIdx.x; u < L1e; u += kThreads) {      // u = (q, i, ab) row-major
+      const int ab = u & 1, i = (u >> 1) % P.npe, q = (u >> 1) / P.npe;
+      const int idx = C == 16 ? ctw_idx<16>(q, i, ab, P.npe) : ctw_idx<8>(q, i, ab, P.npe);
+      sm.ctwe[idx] = tw[q * col_k1(L1e, C, r, 2 * i + ab) * twL_e];
+    }
+    for (int u = threadIdx.x; u < L1p; u += kThreads) {
+      const int ab = u & 1, i = (u >> 1) % P.npp, q = (u >> 1) / P.npp;
+      const int idx = C == 16 ? ctw_idx<16>(q, i, ab, P.npp) : ctw_idx<8>(q, i, ab, P.npp);
+      sm.ctwp[idx] = tw[q * col_k1(L1p, C, r, 2 * i + ab) * twL_p];
+    }
+    if (C == 16) {
+      for (int u = threadIdx.x; u < L1e / 2; u += kThreads)
+        sm.pwe[u] = tw[task_bin(L1e, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(2 * n))];
+      for (int u = threadIdx.x; u < L1p / 2; u += kThreads)
+        sm.pwp[u] = tw[task_bin(L1p, C, int(r), u >> lC, u & (C - 1), 0) * (P.twN / int(n))];
+    } else {                       // task order ((k2 2 + ab) np + i), SpecOp::wtw
+      for (int u = threadIdx.x; u < L1e; u += kThreads) {
+        const int np = P.npe, i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+        sm.pwe[u] = tw[task_bin(L1e, C, int(r), i, k2, ab) * (P.twN / int(2 * n))];
+      }
+      for (int u = threadIdx.x; u < L1p; u += kThreads) {
+        const int np = P.npp, i = u % np, ab = (u / np) & 1, k2 = u / (2 * np);
+        sm.pwp[u] = tw[task_bin(L1p, C, int(r), i, k2, ab) * (P.twN / int(n))];
+      }
+    }
   }
 }
 
@@ -951,7 +982,7 @@ template <int C> struct ColSplit {
 template <int C>
 __device__ __forceinline__ int bix(int q, int t, int ncol, int lnp) {
   using S = ColSplit<C>;
-  if (lnp < 3) return q * ncol + t;
+  if (C < 16 || lnp < 3) return q * ncol + t;   // C < 16: the column-per-thread stage reads rows
   const int key = ((q & (S::T - 1)) | (((t >> lnp) & 1) << S::LT)) << S::SH;
   return q * ncol + (t ^ key);
 }
@@ -993,16 +1024,12 @@ __device__ __forceinline__ void group_transpose(double2 (&x)[Q], int s, unsigned
 template <int C>
 struct PushIn {
   uint32_t bB, aB;
-  int L1, l1, np, ncol, lnp, r, twL;
-  const double2 *rt;                 // resident row twiddles W_L^{r k1} by slot, else nullptr
-  const double2 *tw;
-  __device__ __forceinline__ PushIn(double2 *B, uint64_t *mbB, const Geo &g, uint32_t rr, const double2 *tw_)
+  int L1, l1, np, ncol, lnp, r;
+  __device__ __forceinline__ PushIn(double2 *B, uint64_t *mbB, const Geo &g, uint32_t rr)
       : bB(smem_u32(B)), aB(smem_u32(mbB)), L1(g.L1), l1(g.l1), np(g.np), ncol(g.L1 / C), lnp(g.lnp),
-        r(int(rr)), twL(g.twL), rt(g.ctw), tw(tw_) {}
-  // v times the four-step twiddle W_L^{r k1} of this row, pushed into the owner's B
+        r(int(rr)) {}
   __device__ __forceinline__ void operator()(int p, double2 v) const {
     const int k1 = dperm(p, l1);
-    v = cmul(v, rt ? lds2(rt + p) : tw[r * k1 * twL]);
     int pi, ab;
     if (k1 == 0) { pi = 0; ab = 0; }
     else if (k1 == L1 / 2) { pi = 0; ab = 1; }
@@ -1013,54 +1040,6 @@ struct PushIn {
     push2(mapa_u32(bB + 16u * idx, q), v, mapa_u32(aB, q));
   }
 };
-
-// Receiver's half of the four-step twiddle: slot p of O (bin k1 = dperm(p)) times conj W_L^{r k1}.
-__device__ __forceinline__ double2 orow(const Geo &g, uint32_t r, const double2 *tw, int p) {
-  return g.ctw ? lds2(g.ctw + p) : tw[int(r) * dperm(p, g.l1) * g.twL];
-}
-// First inverse (DIT) stage of a compile-time FFT (radix 4, m = 4, all twiddles 1) on the received
-// slots with the row twiddle applied on the way in; ends synchronized.
-template <int L>
-__device__ __forceinline__ void inv_first_fix(double2 *O, const Geo &g, uint32_t r, const double2 *tw) {
-  for (int b = threadIdx.x; b < L / 4; b += kThreads) {
-    double2 a0 = cmulc(O[pidx(4 * b)], orow(g, r, tw, 4 * b));
-    double2 a1 = cmulc(O[pidx(4 * b + 1)], orow(g, r, tw, 4 * b + 1));
-    double2 a2 = cmulc(O[pidx(4 * b + 2)], orow(g, r, tw, 4 * b + 2));
-    double2 a3 = cmulc(O[pidx(4 * b + 3)], orow(g, r, tw, 4 * b + 3));
-    bfly4<true>(a0, a1, a2, a3);
-    O[pidx(4 * b)] = a0; O[pidx(4 * b + 1)] = a1; O[pidx(4 * b + 2)] = a2; O[pidx(4 * b + 3)] = a3;
-  }
-  __syncthreads();
-}
-// Inverse radix-4 stages m = 2^LM .. 2^LMEND (each followed by a barrier)
-template <int L, int LM, int LMEND>
-struct Ct4InvFrom {
-  __device__ __forceinline__ static void run(double2 *A, const double2 *twd, int L1e) {
-    if constexpr (LM <= LMEND) {
-      st4_ct<true, LM>(A, L, twd, L1e);
-      __syncthreads();
-      Ct4InvFrom<L, LM + 2, LMEND>::run(A, twd, L1e);
-    }
-  }
-};
-// Inverse compile-time FFT of the received O: row twiddles in the first stage, then the rest
-template <int L>
-__device__ __forceinline__ void local_fft_ct_inv_fix(double2 *O, const Geo &g, uint32_t r, const double2 *tw,
-                                                     const double2 *twd, int L1e) {
-  constexpr int l = __builtin_ctz(L), S4 = l / 2;
-  inv_first_fix<L>(O, g, r, tw);
-  Ct4InvFrom<L, 4, 2 * S4>::run(O, twd, L1e);
-  if constexpr (l & 1) {
-    for (int b = threadIdx.x; b < L / 2; b += kThreads) {
-      const int p0 = pidx(b), p1 = pidx(b + L / 2);
-      const double2 a0 = O[p0];
-      const double2 a1 = cmulc(O[p1], twd[b * (L1e / L)]);
-      O[p0] = cadd(a0, a1);
-      O[p1] = csub(a0, a1);
-    }
-    __syncthreads();
-  }
-}
 
 // C > 1, staged: the four-step column stage through the receive buffer B and the output O,
 // both filled by pushes.  Steps: push the local DIF output (slot
@@ -1086,7 +1065,7 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
     mbar_expect(mbO, uint32_t(L1 * 16));
   }
   if (!prepushed) {
-    const PushIn<C> pin(B, mbB, g, r, tw);
+    const PushIn<C> pin(B, mbB, g, r);
 #pragma unroll 4
     for (int p = threadIdx.x; p < L1; p += kThreads) pin(p, A[pidx(p)]);
   }
@@ -1102,6 +1081,91 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
   }
   mbar_wait(mbB, ph);
   TSF_PACC(sm, PS_GATHER);
+  if constexpr (C < 16) {
+    // C <= 8: one thread per column (rows in registers), the bin pairs on all threads through B,
+    // one thread per column for the inverse (measured faster than lane groups at C = 2, 4)
+  for (int t = threadIdx.x; t < ncol; t += kThreads) {        // column DFT_C
+    const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
+    const int k1 = col_k1(L1, C, r, colo);
+    double2 z[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
+    if (g.ctw) {
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], g.ctw[q * ncol + colo]);
+    } else {
+#pragma unroll
+      for (int q = 1; q < C; ++q) z[q] = cmul(z[q], tw[q * k1 * g.twL]);
+    }
+    fft_reg<C, false>(z);
+#pragma unroll
+    for (int q = 0; q < C; ++q) B[q * ncol + t] = z[q];
+  }
+  __syncthreads();
+  TSF_PACC(sm, PS_COLF);
+  // bin pairs: item u = k2 * np + i; regular pair (row k2, col (i,0)) <-> (row C-1-k2, col (i,1)).
+  // The pseudo column pair (0, L1/2) of CTA 0 is done afterwards by warp 0, one pair per lane:
+  // inside the item loop its branch diverged from the regular lanes in every warp and made
+  // CTA 0's stage ~2.4x longer than its peers' (measured), which all of them then waited for.
+  for (int u = threadIdx.x; u < np * C; u += kThreads) {
+    const int k2 = u >> g.lnp, i = u & (np - 1);
+    const int pi = int(r) + i * C;
+    if (pi == 0) continue;
+    const int bin = pi + L1 * k2;
+    double2 &za = B[k2 * ncol + i];
+    double2 &zb = B[(C - 1 - k2) * ncol + np + i];
+    double2 a = za, b = zb;
+    pair_apply(a, b, op.get(k2, 0, i, bin), op.get(C - 1 - k2, 1, i, g.L - bin),
+               op.wtw(k2, 0, i, bin, tw, g.tw2L), op.scale);
+    za = a;
+    zb = b;
+  }
+  if (r == 0 && threadIdx.x < C / 2 + 1 + (C + 1) / 2) {
+    // one bin pair per lane, branch-free (operands selected, a single pair_apply):
+    // column 0 (bins L1 k2): k2 <-> (C - k2) mod C, k2 = 0 with the Nyquist bin;
+    // column L1/2 (bins L1/2 + L1 k2): k2 <-> C - 1 - k2
+    const int o = threadIdx.x;
+    const bool c0 = o <= C / 2;
+    const int k2 = c0 ? o : o - (C / 2 + 1);
+    const int kp = c0 ? (C - k2) % C : C - 1 - k2;
+    const int ab = c0 ? 0 : 1;
+    const int cof = c0 ? 0 : np;
+    const int bin = c0 ? L1 * k2 : L1 / 2 + L1 * k2;
+    const bool self = kp == k2;
+    const double2 la = op.get(k2, ab, 0, bin);
+    const double2 lp = op.get(kp, ab, 0, g.L - bin);
+    const double2 lb = self ? ((c0 && k2 == 0) ? op.nyqe : la) : lp;
+    const double2 w = op.wtw(k2, ab, 0, bin, tw, g.tw2L);
+    double2 &za = B[k2 * ncol + cof];
+    double2 a = za, b = self ? za : B[kp * ncol + cof];
+    pair_apply(a, b, la, lb, w, op.scale);
+    za = a;
+    if (!self) B[kp * ncol + cof] = b;
+  }
+  __syncthreads();
+  TSF_PACC(sm, PS_PAIRS);
+  {
+    const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
+    for (int t = threadIdx.x; t < ncol; t += kThreads) {      // inverse column DFT_C + push back
+      const int ab = t >> g.lnp, i = t & (np - 1), colo = 2 * i + ab;
+      const int k1 = col_k1(L1, C, r, colo);
+      double2 z[C];
+#pragma unroll
+      for (int q = 0; q < C; ++q) z[q] = B[q * ncol + t];
+      fft_reg<C, true>(z);
+      if (g.ctw) {
+#pragma unroll
+        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], g.ctw[q * ncol + colo]);
+      } else {
+#pragma unroll
+        for (int q = 1; q < C; ++q) z[q] = cmulc(z[q], tw[q * k1 * g.twL]);
+      }
+      const uint32_t dst = bO + 16u * uint32_t(pidx(dslot(k1, l1)));
+#pragma unroll
+      for (int q = 0; q < C; ++q) push2(mapa_u32(dst, uint32_t(q)), z[q], mapa_u32(aO, uint32_t(q)));
+    }
+  }
+  } else {
   const int lane = threadIdx.x & (G - 1), ab = lane >> S::LT, s = lane & (T - 1);
   const unsigned gmask = ((1u << G) - 1u) << (lane32 & ~(G - 1));
   const uint32_t bO = smem_u32(O), aO = smem_u32(mbO);
@@ -1114,7 +1178,8 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
     double2 x[Q];
 #pragma unroll
     for (int m = 0; m < Q; ++m) {             // column DFT_C, rows q = s + T m
-      x[m] = B[bix<C>(s + T * m, t, ncol, lnp)];   // row twiddles applied by the sender
+      const int q = s + T * m;
+      x[m] = cmul(B[bix<C>(q, t, ncol, lnp)], g.ctw ? lds2(g.ctw + ctw_idx<C>(q, i, ab, np)) : tw[q * k1 * g.twL]);
     }
     fft_reg<Q, false>(x);
     if constexpr (T > 1) twiddle_tab<C, Q>(x, s, sm.twc);
@@ -1215,10 +1280,12 @@ __device__ __forceinline__ void cross_push(double2 *A, double2 *B, double2 *O, c
     fft_reg<Q, true>(x);
     const uint32_t dst = bO + 16u * uint32_t(pidx(dslot(k1, l1)));
 #pragma unroll
-    for (int m = 0; m < Q; ++m) {             // the receiver applies conj W_L^{q k1} (ofix)
+    for (int m = 0; m < Q; ++m) {
       const int q = s + T * m;
-      push2(mapa_u32(dst, uint32_t(q)), x[m], mapa_u32(aO, uint32_t(q)));
+      const double2 w = g.ctw ? lds2(g.ctw + ctw_idx<C>(q, i, ab, np)) : tw[q * k1 * g.twL];
+      push2(mapa_u32(dst, uint32_t(q)), cmulc(x[m], w), mapa_u32(aO, uint32_t(q)));
     }
+  }
   }
   TSF_PACC(sm, PS_COLI);
   mbar_wait(mbO, ph);
@@ -1501,12 +1568,12 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
   if constexpr (C > 1 && STG) {
 #ifndef TSF_NO_CT_FFT
     if (sm.twd != nullptr && L1e == 1024 && (g.L1 == 1024 || g.L1 == 512)) {
-      const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+      const PushIn<C> pin(sm.B, sm.mbar, g, r);
       if (g.L1 == 1024) local_fft_ct_fwd_out<1024>(sm.A, sm.twd, L1e, pin);
       else local_fft_ct_fwd_out<512>(sm.A, sm.twd, L1e, pin);
       pre = true;
     } else if (sm.twd != nullptr && L1e == 256 && (g.L1 == 256 || g.L1 == 128)) {
-      const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+      const PushIn<C> pin(sm.B, sm.mbar, g, r);
       if (g.L1 == 256) local_fft_ct_fwd_out<256>(sm.A, sm.twd, L1e, pin);
       else local_fft_ct_fwd_out<128>(sm.A, sm.twd, L1e, pin);
       pre = true;
@@ -1542,24 +1609,7 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
     }
     TSF_PTR();
   }
-  if constexpr (C > 1 && STG) {
-    // O still lacks the receiver's row twiddles conj W_L^{r k1}: in the first stage of the
-    // compile-time inverse FFTs, else one pass
-    bool done = false;
-#ifndef TSF_NO_CT_FFT
-    if (sm.twd != nullptr && L1e == 1024 && g.L1 == 1024) { local_fft_ct_inv_fix<1024>(Y, g, r, tw, sm.twd, L1e); done = true; }
-    else if (sm.twd != nullptr && L1e == 1024 && g.L1 == 512) { local_fft_ct_inv_fix<512>(Y, g, r, tw, sm.twd, L1e); done = true; }
-    else if (sm.twd != nullptr && L1e == 256 && g.L1 == 256) { local_fft_ct_inv_fix<256>(Y, g, r, tw, sm.twd, L1e); done = true; }
-    else if (sm.twd != nullptr && L1e == 256 && g.L1 == 128) { local_fft_ct_inv_fix<128>(Y, g, r, tw, sm.twd, L1e); done = true; }
-#endif
-    if (!done) {
-      for (int p = threadIdx.x; p < g.L1; p += kThreads) Y[pidx(p)] = cmulc(Y[pidx(p)], orow(g, r, tw, p));
-      __syncthreads();
-      local_fft<true>(Y, g.L1, sm, L1e);
-    }
-  } else {
-    local_fft<true>(Y, g.L1, sm, L1e);
-  }
+  local_fft<true>(Y, g.L1, sm, L1e);
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
@@ -1662,7 +1712,7 @@ __device__ __forceinline__ void fill_mul(const DevParams &P, const Inst &I, int6
   const int lC = __ffs(C) - 1;
   auto slot_task = [&](int u, int np, int &k2, int &ab, int &i) {
     const int lnp = __ffs(np) - 1;
-    if (res) {
+    if (res && C == 16) {
       ab = u >> (lnp + lC);
       const int k2a = u & (C - 1);
       i = (u >> lC) & (np - 1);
@@ -2140,14 +2190,13 @@ template <int C, int L>
 __device__ __forceinline__ void apply_mid(const Smem &sm, const Geo &g, const SpecOp &op,
                                           const double2 *__restrict__ tw, uint32_t r, Xch &xs) {
   TSF_PT0();
-  const PushIn<C> pin(sm.B, sm.mbar, g, r, tw);
+  const PushIn<C> pin(sm.B, sm.mbar, g, r);
   Ct4Top<L, 4>::run(sm.A, sm.twd, 1024);
   last_stage_out<L>(sm.A, pin);
   TSF_PACC(sm, PS_FFT_F);
   cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs, true);
   TSF_PTR();
-  inv_first_fix<L>(sm.O, g, r, tw);
-  Ct4InvFrom<L, 4, 8>::run(sm.O, sm.twd, 1024);
+  Ct4<true, L, 4>::run(sm.O, sm.twd, 1024);
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;

@@ -211,6 +211,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 struct Smem {
   double2 *A, *B, *O;
   double2 *twd, *thi, *tlo;          // twd != nullptr: direct table
+  double2 *tws;                      // per-stage twiddles of the compile-time FFTs (L1e = 1024 / 256), tws_len
   double2 *ctwe, *ctwp;              // column twiddles (resident)
   double2 *mule, *mulp, *pwe, *pwp;  // per-level multipliers lambda_A, 1/lambda_P / pair twiddles (resident)
   double2 *vs;                       // Krylov vectors of this CTA's chunk (kSmemVec x L1p), or null
@@ -273,6 +274,7 @@ __device__ __forceinline__ Smem smem_view(unsigned char *raw, int L1e, int L1p, 
     s.thi = c; c += tw_hi_len(L1e);
     s.tlo = c; c += tw_lo_len(L1e);
   }
+  if (resident && (L1e == 1024 || L1e == 256)) { s.tws = c; c += tws_len(L1e); }
   if (vsmem) { s.vs = c; c += kSmemVec * L1p; }
   double *d = reinterpret_cast<double *>(c);
   s.wred = d;
@@ -320,6 +322,17 @@ __device__ __forceinline__ void load_constants(const DevParams &P, const double2
   }
   if (C > 1)
     for (int e = threadIdx.x; e < C; e += kThreads) sm.twc[e] = tw[e * (P.twN / C)];
+  if (sm.tws) {
+    // per-stage tables (conflict-free: a stage's lanes read consecutive entries): stage m = 2^LM
+    // holds W_m^k, k < m / 4, at (L1e - m) / 3; then W_{L1e/2}^b, b < L1e / 4 (the radix-2 stage)
+    const int nst = (L1e - 1) / 3;
+    for (int u = threadIdx.x; u < tws_len(L1e); u += kThreads) {
+      if (u >= nst) { sm.tws[u] = tw[(u - nst) * (P.twN / (L1e / 2))]; continue; }
+      int lm = __ffs(L1e) - 1;
+      while (u >= (L1e - (1 << (lm - 2))) / 3) lm -= 2;
+      sm.tws[u] = tw[(u - (L1e - (1 << lm)) / 3) * (P.twN >> lm)];
+    }
+  }
   if (sm.ctwe) {
     // resident tables in the layouts of the staged column stage (cross_push): column twiddles
     // W_L^{q k1} at ctw_idx(q, i, ab), pair twiddles W_{2L}^{bin} of the a-side bins
@@ -598,14 +611,13 @@ __device__ __forceinline__ void fft_pass16(double2 *A, int L1, int lm, const Sme
 template <bool INV, int LM>
 __device__ __forceinline__ void st4_ct(double2 *A, int L1, const double2 *twd, int L1e) {
   constexpr int lmp = LM - 2, mprev = 1 << lmp;
-  const int tstep = L1e >> LM;
   const int nb = L1 >> 2;
   for (int b = threadIdx.x; b < nb; b += kThreads) {
     const int k = b & (mprev - 1);
     const int base = ((b >> lmp) << LM) + k;
     const int p0 = pidx(base), p1 = pidx(base + mprev), p2 = pidx(base + 2 * mprev), p3 = pidx(base + 3 * mprev);
     double2 a0 = A[p0], a1 = A[p1], a2 = A[p2], a3 = A[p3];
-    const double2 w1 = twd[k * tstep];
+    const double2 w1 = twd[(L1e - (1 << LM)) / 3 + k];   // per-stage table (tws)
     const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
     if (INV) {
       a1 = cmulc(a1, w1); a2 = cmulc(a2, w2); a3 = cmulc(a3, w3);
@@ -643,7 +655,7 @@ __device__ __forceinline__ void local_fft_ct(double2 *A, const double2 *twd, int
         const int p0 = pidx(b), p1 = pidx(b + L / 2);
         const double2 a0 = A[p0], a1 = A[p1];
         A[p0] = cadd(a0, a1);
-        A[p1] = cmul(csub(a0, a1), twd[b * (L1e / L)]);
+        A[p1] = cmul(csub(a0, a1), twd[(L1e - 1) / 3 + b]);
       }
       __syncthreads();
     }
@@ -654,7 +666,7 @@ __device__ __forceinline__ void local_fft_ct(double2 *A, const double2 *twd, int
       for (int b = threadIdx.x; b < L / 2; b += kThreads) {
         const int p0 = pidx(b), p1 = pidx(b + L / 2);
         const double2 a0 = A[p0];
-        const double2 a1 = cmulc(A[p1], twd[b * (L1e / L)]);
+        const double2 a1 = cmulc(A[p1], twd[(L1e - 1) / 3 + b]);
         A[p0] = cadd(a0, a1);
         A[p1] = csub(a0, a1);
       }
@@ -709,7 +721,7 @@ __device__ __forceinline__ void local_fft_ct_fwd_out(double2 *A, const double2 *
       const int p0 = pidx(b), p1 = pidx(b + L / 2);
       const double2 a0 = A[p0], a1 = A[p1];
       A[p0] = cadd(a0, a1);
-      A[p1] = cmul(csub(a0, a1), twd[b * (L1e / L)]);
+      A[p1] = cmul(csub(a0, a1), twd[(L1e - 1) / 3 + b]);
     }
     __syncthreads();
   }
@@ -723,13 +735,13 @@ __device__ __forceinline__ void local_fft_ct_fwd_out(double2 *A, const double2 *
 template <bool INV>
 __device__ __forceinline__ void local_fft(double2 *A, int L1, const Smem &sm, int L1e) {
 #ifndef TSF_NO_CT_FFT
-  if (sm.twd != nullptr && L1e == 1024) {       // C3's resident cluster kernels (n = 2^14, C = 16)
-    if (L1 == 1024) { local_fft_ct<INV, 1024>(A, sm.twd, L1e); return; }
-    if (L1 == 512) { local_fft_ct<INV, 512>(A, sm.twd, L1e); return; }
+  if (sm.tws != nullptr && L1e == 1024) {       // C3's resident cluster kernels (n = 2^14, C = 16)
+    if (L1 == 1024) { local_fft_ct<INV, 1024>(A, sm.tws, L1e); return; }
+    if (L1 == 512) { local_fft_ct<INV, 512>(A, sm.tws, L1e); return; }
   }
-  if (sm.twd != nullptr && L1e == 256) {        // C2's (n = 2^10, C = 4)
-    if (L1 == 256) { local_fft_ct<INV, 256>(A, sm.twd, L1e); return; }
-    if (L1 == 128) { local_fft_ct<INV, 128>(A, sm.twd, L1e); return; }
+  if (sm.tws != nullptr && L1e == 256) {        // C2's (n = 2^10, C = 4)
+    if (L1 == 256) { local_fft_ct<INV, 256>(A, sm.tws, L1e); return; }
+    if (L1 == 128) { local_fft_ct<INV, 128>(A, sm.tws, L1e); return; }
   }
 #endif
   const int l = __ffs(L1) - 1;
@@ -1567,15 +1579,15 @@ __device__ TSF_APPLY_ATTR double2 *apply_smem(const Smem &sm, int L1e, const Geo
   bool pre = false;               // forward FFT already pushed its outputs (staged, compile-time FFT)
   if constexpr (C > 1 && STG) {
 #ifndef TSF_NO_CT_FFT
-    if (sm.twd != nullptr && L1e == 1024 && (g.L1 == 1024 || g.L1 == 512)) {
+    if (sm.tws != nullptr && L1e == 1024 && (g.L1 == 1024 || g.L1 == 512)) {
       const PushIn<C> pin(sm.B, sm.mbar, g, r);
-      if (g.L1 == 1024) local_fft_ct_fwd_out<1024>(sm.A, sm.twd, L1e, pin);
-      else local_fft_ct_fwd_out<512>(sm.A, sm.twd, L1e, pin);
+      if (g.L1 == 1024) local_fft_ct_fwd_out<1024>(sm.A, sm.tws, L1e, pin);
+      else local_fft_ct_fwd_out<512>(sm.A, sm.tws, L1e, pin);
       pre = true;
-    } else if (sm.twd != nullptr && L1e == 256 && (g.L1 == 256 || g.L1 == 128)) {
+    } else if (sm.tws != nullptr && L1e == 256 && (g.L1 == 256 || g.L1 == 128)) {
       const PushIn<C> pin(sm.B, sm.mbar, g, r);
-      if (g.L1 == 256) local_fft_ct_fwd_out<256>(sm.A, sm.twd, L1e, pin);
-      else local_fft_ct_fwd_out<128>(sm.A, sm.twd, L1e, pin);
+      if (g.L1 == 256) local_fft_ct_fwd_out<256>(sm.A, sm.tws, L1e, pin);
+      else local_fft_ct_fwd_out<128>(sm.A, sm.tws, L1e, pin);
       pre = true;
     }
 #endif
@@ -2150,10 +2162,10 @@ enum LevelState { S_RHS = 0, S_WARM = 1, S_TRUE = 2, S_KRYLOV = 3 };
 // unfused loop (R-fuse); one barrier and one shared-memory round trip fewer per stage boundary.
 namespace fz {
 constexpr int kH = kThreads;        // e = b and b + kH (npc = 512)
-// P^{-1} forward, first stage (radix 2, L = 512, twiddle W_512^b = twd[2b])
+// P^{-1} forward, first stage (radix 2, L = 512, twiddle W_512^b = tws[341 + b]); twd below is sm.tws
 __device__ __forceinline__ void p_first(double2 *A, int b, double2 a0, double2 a1, const double2 *twd) {
   A[pidx(b)] = cadd(a0, a1);
-  A[pidx(b + kH)] = cmul(csub(a0, a1), twd[2 * b]);
+  A[pidx(b + kH)] = cmul(csub(a0, a1), twd[341 + b]);   // tws: W_512^b
 }
 // A forward, first stage (radix 4, m = 1024) on the zero-padded input (a2 = a3 = 0)
 __device__ __forceinline__ void a_first(double2 *A, int b, double2 a0, double2 a1, const double2 *twd) {
@@ -2167,7 +2179,7 @@ __device__ __forceinline__ void a_first(double2 *A, int b, double2 a0, double2 a
 // P^{-1} inverse, last stage (radix 2): elements b, b + 256
 __device__ __forceinline__ void p_last(const double2 *O, int b, const double2 *twd, double2 &o0, double2 &o1) {
   const double2 a0 = O[pidx(b)];
-  const double2 a1 = cmulc(O[pidx(b + kH)], twd[2 * b]);
+  const double2 a1 = cmulc(O[pidx(b + kH)], twd[341 + b]);
   o0 = cadd(a0, a1);
   o1 = csub(a0, a1);
 }
@@ -2191,12 +2203,12 @@ __device__ __forceinline__ void apply_mid(const Smem &sm, const Geo &g, const Sp
                                           const double2 *__restrict__ tw, uint32_t r, Xch &xs) {
   TSF_PT0();
   const PushIn<C> pin(sm.B, sm.mbar, g, r);
-  Ct4Top<L, 4>::run(sm.A, sm.twd, 1024);
+  Ct4Top<L, 4>::run(sm.A, sm.tws, 1024);
   last_stage_out<L>(sm.A, pin);
   TSF_PACC(sm, PS_FFT_F);
   cross_push<C>(sm.A, sm.B, sm.O, g, op, tw, r, sm, xs, true);
   TSF_PTR();
-  Ct4<true, L, 4>::run(sm.O, sm.twd, 1024);
+  Ct4<true, L, 4>::run(sm.O, sm.tws, 1024);
   TSF_PACC(sm, PS_FFT_I);
 #ifdef TSF_PROFILE
   if (threadIdx.x == 0 && blockIdx.x == TSF_PROF_CTA) sm.prof[PS_APPLIES] += 1;
@@ -2215,7 +2227,7 @@ __device__ __forceinline__ void bicg_fused(const DevParams &P, const Smem &sm, c
   using namespace fz;
   double2 *__restrict__ X = V.X, *__restrict__ R = V.R, *__restrict__ RH = V.RH, *__restrict__ PV = V.P;
   double2 *__restrict__ VV = V.V, *__restrict__ S = V.S, *__restrict__ PH = V.PH, *__restrict__ SH = V.SH;
-  const double2 *twd = sm.twd;
+  const double2 *twd = sm.tws;
   double2 *A = sm.A, *O = sm.O;
   const int b = threadIdx.x, b1 = threadIdx.x + kH;
   double rho = rr0, alpha = 0.0, omega = 0.0, beta = 0.0, ssp = 0.0;
@@ -2441,7 +2453,7 @@ __device__ __forceinline__ void level_solve(const DevParams &P, const Inst &I, c
 
     bool fused = false;
     if constexpr (METHOD == TSF_BICGSTAB && C == 16 && STG && !BIG) {
-      if (iterate && P.fuse && prec && !P.pipelined && sm.twd != nullptr && sm.vs != nullptr &&
+      if (iterate && P.fuse && prec && !P.pipelined && sm.tws != nullptr && sm.vs != nullptr &&
           P.L1e == 1024 && P.L1p == 512) {
         bicg_fused<C>(P, sm, V, ge, gp, opA, opP, tw, r, xs, rr0, rn0, hs, relres, status);
         fused = true;

@@ -158,12 +158,16 @@ DevParams dev_params(const Plan &pl, char *ws);
 // [L1e/64 + 64]), resident tables: column twiddles [L1e + L1p], per-level multipliers
 // [L1e + L1p], pair twiddles [L1e + L1p] (double2), Krylov vectors [kSmemVec x L1p] (double2) if
 // vsmem; 48 doubles of reduction scratch, 128 doubles of pushed CTA partials and 4 mbarriers.
+// Per-stage twiddle table of the compile-time local FFTs (resident, L1e = 1024 or 256): stage
+// tables of W_m^k (k < m/4) for m = 4 .. L1e, then W_{L1e/2}^b (b < L1e/4).
+TSF_HD inline int tws_len(int64_t L1e) { return (L1e == 1024 || L1e == 256) ? int((L1e - 1) / 3 + L1e / 4) : 0; }
 TSF_HD inline int64_t smem_bytes(int64_t L1e, int64_t L1p, int staged, int resident, int vsmem,
                                  int64_t chunk_cplx = 0) {
   // A holds one row of at most kMaxLocal points (multi-pass regime: L1e > kMaxLocal)
   const int64_t la = L1e > kMaxLocal ? kMaxLocal : L1e;
   int64_t c2 = (staged ? 3 * la : la) + (staged ? 2 : 1) * kPadBuf * (la / 16);   // A (+ B, O)
   if (resident) c2 += L1e + 3 * (L1e + L1p);      // twiddles, column twiddles, multipliers, pair twiddles
+  if (resident) c2 += tws_len(L1e);                // per-stage twiddles of the compile-time FFTs
   else c2 += (L1e >= 64 ? L1e / 64 : 1) + (L1e >= 64 ? 64 : L1e);
   if (vsmem) c2 += kSmemVec * L1p;
   if (!staged) c2 += chunk_cplx;                   // chunk buffer of the unstaged column stage

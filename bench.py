@@ -237,12 +237,16 @@ def oracle_rate(cfg):
 
 
 def lib_hash() -> str:
+    """Identity of the kernel build the ncu traffic belongs to: sha256 over the library's sources,
+    headers and compile flags (a rebuild of the same sources links a different binary image, so
+    the .so bytes themselves are not a stable key)."""
     import hashlib
-    from paper_1603_00279_b200 import _lib as L
+    from paper_1603_00279_b200 import build as B
     h = hashlib.sha256()
-    with open(L.LIB_PATH, "rb") as fh:
-        for chunk in iter(lambda: fh.read(1 << 24), b""):
-            h.update(chunk)
+    h.update(" ".join(B.FLAGS).encode())
+    for f in sorted(B.SOURCES + B.HEADERS):
+        with open(os.path.join(B.CSRC, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
     return h.hexdigest()[:16]
 
 

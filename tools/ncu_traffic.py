@@ -1,6 +1,6 @@
 """Capture the DRAM traffic of bench.py's timed k_solve launch with ncu and record it in
-profiles/traffic.json keyed by workload and the sha256 of libtsf.so (bench.py refuses entries
-captured with another library build).  Run on the GPU box:
+profiles/traffic.json keyed by workload and the sha256 of the library's sources and compile flags
+(bench.py refuses entries captured with other kernel sources).  Run on the GPU box:
 
     python tools/ncu_traffic.py C3 [C4 C5 ...] [--method bicgstab] [--out profiles/traffic.json]
 

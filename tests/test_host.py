@@ -237,3 +237,28 @@ def test_gather_over_two_gloo_ranks_equals_single_rank(tmp_path):
     np.testing.assert_array_equal(got[: 45], np.array(ref).ravel())
     # rank 0 owns instances {0, 1}, rank 1 owns {2}: iteration rows tag the owner
     np.testing.assert_array_equal(got[45:], [2] * 12 + [4] * 6)
+
+
+def test_ncu_traffic_key_is_a_hash_of_the_kernel_sources(tmp_path, monkeypatch):
+    """bench.py accepts an ncu DRAM-traffic capture only for the kernel sources it was taken
+    with: the key is a hash over csrc/ + include/tsf.h + compile flags (stable across rebuilds of
+    the same sources, different as soon as a source byte or a flag changes)."""
+    import shutil
+
+    import bench
+    from paper_1603_00279_b200 import build as B
+    h0 = bench.lib_hash()
+    assert re.fullmatch(r"[0-9a-f]{16}", h0) and bench.lib_hash() == h0
+    d = tmp_path / "a" / "b" / "csrc"
+    d.mkdir(parents=True)
+    (tmp_path / "a" / "include").mkdir()
+    for f in B.SOURCES + B.HEADERS:
+        shutil.copy(os.path.join(B.CSRC, f), os.path.normpath(os.path.join(d, f)))
+    monkeypatch.setattr(B, "CSRC", str(d))
+    assert bench.lib_hash() == h0
+    with open(d / "tsf_plan.cpp", "a") as fh:
+        fh.write("\n")
+    assert bench.lib_hash() != h0
+    monkeypatch.setattr(B, "CSRC", os.path.join(os.path.dirname(B.__file__), "csrc"))
+    monkeypatch.setattr(B, "FLAGS", B.FLAGS + ["-DX"])
+    assert bench.lib_hash() != h0

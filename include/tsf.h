@@ -81,7 +81,9 @@ typedef void (*tsf_src_cb)(const double *x, int64_t n, double t, double *out, vo
  *   TSF_SRC_ZERO      f = 0
  *   TSF_SRC_SEPARABLE f^{j+sigma} = sum_{k<K} scal[j*K+k] * basis[k*n+i], 1 <= K <= 4
  *   TSF_SRC_TABLE     f^{j+sigma}_i = f_table[j*n+i]  (M x n, natural order): a host array
- *                     (copied at init), or with f_table_on_device = 1 a device array of the
+ *                     (copied at init on the handle's stream, directly from this buffer:
+ *                     pinned memory makes it one DMA per instance; the copy has completed when
+ *                     tsf_init returns), or with f_table_on_device = 1 a device array of the
  *                     handle's device that is BORROWED (read every level; must stay valid and
  *                     unchanged until tsf_destroy; all instances of a handle agree on the flag)
  *   TSF_SRC_CALLBACK  f^{j+sigma} = f_cb(x, n, t_{j+sigma}) evaluated on the host once per level

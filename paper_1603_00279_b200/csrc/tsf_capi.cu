@@ -201,6 +201,17 @@ __global__ void k_reset(DevParams P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *P.level = 0;
 }
 
+// Host source table (eq3.1 f^{j+sigma}): rows arrive in natural order (staged in the
+// instance's still-unused history block) and are stored in the chunk order of the kernels.
+__global__ void k_permute_rows(const double *__restrict__ nat, double *__restrict__ out, int64_t n, int64_t M, int C) {
+  const int64_t total = n * M;
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = id / n, e = id % n;
+    out[j * n + perm_pos(n, C, e)] = nat[id];
+  }
+}
+
 // Nonsingularity guard of the circulant preconditioner (themx2 P:831-848 proves
 // P nonsingular in exact arithmetic): for every (instance, level) block, min and max |lambda_P|
 // over the n/2 + 1 bins of the level's spectrum; |lambda_P| < 1e-14 max |lambda_P| marks the
@@ -509,20 +520,26 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
   CKH(cudaGetLastError());
 
   // Per-instance inputs.  Every host-provided field of an instance block lies in [0, o_omega)
-  // (par, level tables, history weights, source, phi): they are written into ONE host image of
-  // B x o_omega bytes (permuted chunks where the kernels want them) and uploaded by a single
-  // pitched copy on the handle's stream, ordered after the zeroing memset above (pageable
-  // source: cudaMemcpy2DAsync returns once the image is staged, so it may be freed after).
-  // u^0 = phi is then set on the device by k_reset.  A device f table is borrowed (R-ftab).
+  // (par, level tables, history weights, source, phi): they are written into ONE host image per
+  // instance (permuted chunks where the kernels want them) and uploaded by pitched copies on the
+  // handle's stream, ordered after the zeroing memset above (pageable source: cudaMemcpy2DAsync
+  // returns once the image is staged, so it may be freed after).  A host f table (the bulk of
+  // the input: M x n doubles) is left out of the image: it goes straight from the caller's
+  // buffer (one DMA per instance when that buffer is pinned) into the instance's history
+  // block, which nothing reads before level 1, and k_permute_rows moves it into the table in
+  // chunk order; the history block is zeroed again afterwards.  u^0 = phi is then set on the
+  // device by k_reset.  A device f table is borrowed (R-ftab).
   {
-    const size_t img = size_t(pl.o_omega);
+    const bool tab_host = pl.src_kind == TSF_SRC_TABLE && !pl.ftab_dev && p[0].src_kind == TSF_SRC_TABLE;
+    const int64_t gap = tab_host ? int64_t(pl.o_phi) - int64_t(pl.o_ftab) : 0;   // table bytes left out
+    const size_t img = size_t(int64_t(pl.o_omega) - gap);
     std::vector<char> himg(img * size_t(B), 0);
     std::vector<double> tmp(static_cast<size_t>(std::max<int64_t>(n, 8))), xs(static_cast<size_t>(n));
     std::vector<double> tl(static_cast<size_t>(M));
     for (int32_t b = 0; b < B; ++b) {
       const tsf_problem &q = p[b];
       char *base = himg.data() + size_t(b) * img;
-      auto at = [&](int64_t off) { return reinterpret_cast<double *>(base + off); };
+      auto at = [&](int64_t off) { return reinterpret_cast<double *>(base + (off >= int64_t(pl.o_phi) ? off - gap : off)); };
       InstTables T;
       inst_tables(q, &T);
       double par[16] = {T.sigma, q.beta, 0.0, T.kappa, T.h, T.tau, 0.0, 0.0};
@@ -540,8 +557,8 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
       if (q.src_kind == TSF_SRC_SEPARABLE) {
         std::memcpy(at(pl.o_scal), q.scal, size_t(M) * size_t(pl.K) * 8);
         for (int k = 0; k < pl.K; ++k) permute_host(n, pl.C, q.basis + int64_t(k) * n, at(pl.o_basis) + int64_t(k) * n);
-      } else if (q.src_kind == TSF_SRC_TABLE && !pl.ftab_dev) {
-        for (int64_t j = 0; j < M; ++j) permute_host(n, pl.C, q.f_table + j * n, at(pl.o_ftab) + j * n);
+      } else if (q.src_kind == TSF_SRC_TABLE) {
+        // host table: uploaded below from the caller's buffer; device table: borrowed
       } else if (q.src_kind == TSF_SRC_CALLBACK) {
         // slow path: the host callback is evaluated once per level at
         // t_{j+sigma} here, into the instance's source table (same kernel path as a table)
@@ -556,8 +573,24 @@ int tsf_init(const tsf_problem *p, int32_t B, const tsf_solver *s, void *d_ws, s
         }
       }
     }
-    CKH(cudaMemcpy2DAsync(h->ws + pl.off_inst, pl.stride, himg.data(), img, img, size_t(B),
-                          cudaMemcpyHostToDevice, st));
+    if (!tab_host) {
+      CKH(cudaMemcpy2DAsync(h->ws + pl.off_inst, pl.stride, himg.data(), img, img, size_t(B),
+                            cudaMemcpyHostToDevice, st));
+    } else {
+      CKH(cudaMemcpy2DAsync(h->ws + pl.off_inst, pl.stride, himg.data(), img, size_t(pl.o_ftab), size_t(B),
+                            cudaMemcpyHostToDevice, st));
+      CKH(cudaMemcpy2DAsync(h->ws + pl.off_inst + pl.o_phi, pl.stride, himg.data() + size_t(pl.o_ftab), img,
+                            size_t(pl.o_omega - pl.o_phi), size_t(B), cudaMemcpyHostToDevice, st));
+      const size_t tab = size_t(M) * size_t(n) * 8;
+      for (int32_t b = 0; b < B; ++b) {
+        char *blk = h->ws + pl.off_inst + size_t(b) * pl.stride;
+        CKH(cudaMemcpyAsync(blk + pl.o_hist, p[b].f_table, tab, cudaMemcpyHostToDevice, st));
+        k_permute_rows<<<grid_for(M * n), 256, 0, st>>>(reinterpret_cast<const double *>(blk + pl.o_hist),
+                                                        reinterpret_cast<double *>(blk + pl.o_ftab), n, M, pl.C);
+        CKH(cudaMemsetAsync(blk + pl.o_hist, 0, tab, st));
+      }
+      CKH(cudaGetLastError());
+    }
     if (pl.ftab_dev) {
       std::vector<const double *> ptrs(static_cast<size_t>(B));
       for (int32_t b = 0; b < B; ++b) ptrs[size_t(b)] = p[b].f_table;

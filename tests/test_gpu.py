@@ -557,6 +557,32 @@ def test_callback_and_device_table_sources_equal_the_host_table():
     assert max_rel(outs[0], O.solve(p)) <= RTOL
 
 
+def test_host_tables_pinned_batched_on_a_side_stream_equal_the_oracle():
+    """tsf_init DMAs a host f table from the caller's buffer into the (still unused) history block
+    and permutes it on the device: pinned and pageable tables, a batch of two instances with
+    different tables and a handle stream with work queued must all give the oracle's solution
+    (eq3.1) and the same bits."""
+    import torch
+    rng = np.random.default_rng(5)
+    base = dict(alpha=0.7, beta=1.6, n=1024, M=12, gamma=const(0.3), dplus=const(1.1), dminus=const(0.6))
+    tabs = [rng.standard_normal((12, 1024)) for _ in range(2)]
+    ref = tsf.Solver([Instance(**base, source="table", f_table=tb) for tb in tabs], cluster=4)
+    u_ref = run_levels(ref, 12)
+    pins = [torch.from_numpy(tb.copy()).pin_memory() for tb in tabs]
+    st = torch.cuda.Stream()
+    big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(st):
+        for _ in range(8):
+            big.fill_(1)
+    s = tsf.Solver([Instance(**base, source="table", f_table=pt.numpy()) for pt in pins], cluster=4, stream=st)
+    u = run_levels(s, 12)
+    for b in range(2):
+        np.testing.assert_array_equal(u[b], u_ref[b])
+        p = O.Problem(alpha=0.7, beta=1.6, n=1024, M=12, gamma=(O.CONST, 0.3), dplus=(O.CONST, 1.1),
+                      dminus=(O.CONST, 0.6), src=O.SRC_TABLE, f_table=tabs[b])
+        assert max_rel(u[b], O.solve(p)) <= RTOL
+
+
 def test_singular_preconditioner_is_rejected_at_init():
     """|lambda_P| < 1e-14 max |lambda_P| is singular.  With d+- = 0, bin 0 of lambda_P
     is eta_j alone; T = 1e30, alpha = 1 make eta ~ 1e-30 against |gamma|/h ~ 1e2."""

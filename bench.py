@@ -485,6 +485,7 @@ def main():
             "krylov_iters_per_s": iters_per_s,
             "mean_iters_per_level": iters_job / levels_job,
             "init_s": t_init,
+            "init_split_s": {"marshal_python": s.marshal_s, "tsf_init": s.init_s},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "k_solve (one launch = all M levels of the rank's batch)",

@@ -6,6 +6,7 @@ provides the device workspace and the CUDA stream.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from typing import Sequence
 
 import numpy as np
@@ -120,7 +121,9 @@ class Solver:
         self.instances = list(instances)
         self.B = len(self.instances)
         self.n, self.M = self.instances[0].n, self.instances[0].M
+        t0 = time.perf_counter()
         probs, keep = marshal(self.instances)
+        self.marshal_s = time.perf_counter() - t0      # host arrays from the Instance specs (Python)
         self.h2d_bytes = sum(a.nbytes for arrs in keep for a in arrs.values() if isinstance(a, np.ndarray))
         self._borrowed = [arrs["f_dev"] for arrs in keep if "f_dev" in arrs]
         self._solver = make_solver_struct(method, precond, tol, maxit, cluster, x0_warm, true_residual,
@@ -140,9 +143,11 @@ class Solver:
             # from reusing it while the handle's kernels may still run
             self.workspace.record_stream(self.stream)
         h = C.c_void_p()
+        t0 = time.perf_counter()
         L.check(self.lib.tsf_init(probs, self.B, C.byref(self._solver),
                                   C.c_void_p(self.workspace.data_ptr()), C.c_size_t(int(info.workspace_bytes)),
                                   dev.index, C.c_void_p(self.stream.cuda_stream), C.byref(h)), "tsf_init")
+        self.init_s = time.perf_counter() - t0         # the C-ABI tsf_init call (uploads + setup kernels)
         self.h = h
         del keep
 
